@@ -1,0 +1,104 @@
+/*
+ * permanent_b200.h -- C ABI of the B200 exact-permanent engine
+ * (libpermanent_b200.so, built from paper_2510_03421_b200/csrc/).
+ *
+ * The reference package (`permanent`, /root/reference/pkg/src/permanent) has
+ * no native boundary: its engine seam is the kernel registry
+ * `_kernels.get_kernel(name, compiled)` (src/_kernels.py:718-728), whose
+ * callables are invoked only from the wrappers in src/algorithms.py
+ * (:87-89, 104-106, 133-136, 152-159, 175-182).  Every entry point below
+ * replaces one of those kernels *plus* its wrapper's normalization, so the
+ * Python shim (paper_2510_03421_b200/) keeps the reference's public API
+ * (src/__init__.py:55-111) and calls straight through.  Paths are relative to
+ * /root/reference/pkg.
+ *
+ * Conventions
+ *   - matrices are row-major m x n with row stride `lda` elements, m <= n
+ *     (the caller transposes, as src/__init__.py:50-52 does);
+ *   - complex128 is interleaved (re, im) doubles: numpy's complex128 layout;
+ *   - `dev_ptr` = 1: `a` is a device pointer on the current device (read in
+ *     place); 0: host memory (copied; never written);
+ *   - `stream` is a cudaStream_t (NULL = per-thread default stream); calls
+ *     that return a host value synchronize that stream;
+ *   - every function returns a status:
+ */
+#ifndef PERMANENT_B200_H
+#define PERMANENT_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PERM_OK = 0,
+  PERM_OVERFLOW = 1,   /* int: an int64 intermediate overflowed (reference semantics)
+                          or the exact value is not certified to fit */
+  PERM_BAD_SHAPE = 2,  /* m > n, m < 1, n > 62, unsupported size */
+  PERM_BUDGET = 3,     /* combinatoric step budget exceeded */
+  PERM_CUDA = 4,       /* CUDA / NCCL runtime error (see perm_last_error) */
+  PERM_BAD_ARG = 5
+};
+
+/* algorithm ids, same order as AlgorithmId in src/algorithms.py:26-31 */
+enum { PERM_ALG_COMBINATORIC = 0, PERM_ALG_RYSER = 1, PERM_ALG_GLYNN = 2 };
+
+/* Library version (major*10000 + minor*100 + patch). */
+int perm_version(void);
+/* Message of the last failing call on this host thread ("" if none). */
+const char* perm_last_error(void);
+/* Select the CUDA device used by subsequent calls from this host thread. */
+int perm_set_device(int device);
+/* Number of SMs of the current device (planning helper). */
+int perm_device_sm_count(void);
+
+/* ---- single permanents, float64 / complex128 --------------------------
+ * Replace glynn_sq/glynn_rect + permanent_glynn_{square,rectangular}
+ * (src/_kernels.py:373-409, 531-577; src/algorithms.py:140-184):
+ * `out` receives the *normalized* permanent (1 double, or re/im for c128).
+ * Rectangular Glynn pre-scales the real rows by a power of two
+ * (SURVEY 7.4.2), which is exact algebra.  `magsum` (optional, may be NULL)
+ * receives M = the normalized sum of |terms|. */
+int perm_glynn_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
+                   void* stream);
+int perm_glynn_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
+                    void* stream);
+/* Replace ryser_sq / ryser_rect + permanent_ryser_{square,rectangular}
+ * (src/_kernels.py:115-145, 226-262; src/algorithms.py:93-137).  The
+ * rectangular form walks all 2^n column subsets with the binomial weight of
+ * each subset size (src/algorithms.py:110-115). */
+int perm_ryser_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
+                   void* stream);
+int perm_ryser_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
+                    void* stream);
+
+/* ---- sharded walks (one Gray range per GPU / rank) --------
+ * perm_walk_steps: length of the Gray index space of (alg, m, n): 2^(n-1)
+ * for Glynn, 2^n for Ryser.  perm_walk_shard: the [k_begin, k_end) of
+ * `rank` out of `world`, aligned so every shard runs the full-speed kernel.
+ * perm_walk_partial_*: raw compensated partial sum over one range, written
+ * as 8 doubles {re_hi, re_lo, im_hi, im_lo, mag, 0, 0, 0} to `partial`
+ * (host memory, or device memory when partial_on_device = 1, in which case
+ * the call is asynchronous on `stream`).
+ * perm_walk_finish_*: combine G partials in rank order (double-double) and
+ * apply the algorithm's normalization -> the permanent (and M). */
+uint64_t perm_walk_steps(int alg, int m, int n);
+int perm_walk_shard(int alg, int m, int n, int rank, int world, uint64_t* k_begin, uint64_t* k_end);
+int perm_walk_partial_f64(int alg, int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t k_begin,
+                          uint64_t k_end, int mag, double* partial, int partial_on_device, void* stream);
+int perm_walk_partial_c128(int alg, int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t k_begin,
+                           uint64_t k_end, int mag, double* partial, int partial_on_device, void* stream);
+int perm_walk_finish_f64(int alg, int m, int n, const double* a, int64_t lda, const double* partials, int G,
+                         double* out, double* magsum);
+int perm_walk_finish_c128(int alg, int m, int n, const double* a, int64_t lda, const double* partials, int G,
+                          double* out, double* magsum);
+
+/* ---- dispatch (src/dispatch.py:84-95) -----------------------------------
+ * The reference's selection rule over (m, n) with parameters p[0..7] =
+ * p1..p8; returns PERM_ALG_*.  batch/ngpu are reserved (0). */
+int perm_select(int m, int n, const double* p, int64_t batch, int ngpu);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PERMANENT_B200_H */

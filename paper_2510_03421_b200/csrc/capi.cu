@@ -1,0 +1,232 @@
+// extern "C" entry points of libpermanent_b200.so (include/permanent_b200.h).
+#include <algorithm>
+
+#include "engine.cuh"
+
+using namespace permb200;
+
+namespace permb200 {
+const char* last_error();
+}
+
+namespace {
+
+int check_shape(int alg, int m, int n) {
+  if (m < 1 || n < 1) {
+    set_error("matrix must have m >= 1 and n >= 1");
+    return PERM_BAD_SHAPE;
+  }
+  if (m > n) {
+    set_error("need m <= n; transpose first");
+    return PERM_BAD_SHAPE;
+  }
+  // src/algorithms.py:47 caps subset / sign walks at 62 columns; the device
+  // kernels hold the state vector in registers, up to 64 entries.
+  if (n > 62) {
+    set_error("walk over more than 62 columns");
+    return PERM_BAD_SHAPE;
+  }
+  (void)alg;
+  return PERM_OK;
+}
+
+// Single permanent through the walk engine; returns normalized value.
+int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out,
+                double* magsum, void* stream_) {
+  clear_error();
+  int st = check_shape(alg, m, n);
+  if (st) return st;
+  cudaStream_t stream = pick_stream(stream_);
+  HostMat A;
+  st = load_matrix(m, n, a, lda, dev_ptr, cplx, &A, stream);
+  if (st) return st;
+  WalkSetup ws;
+  st = build_walk(alg, A, &ws);
+  if (st) return st;
+  Scratch* s = scratch();
+  if (!s) return cuda_fail(cudaErrorNoDevice, "scratch");
+  // result slot: reserve 8 doubles after the walk data in scratch
+  const size_t part_bytes = (size_t)kMaxPartials * kPartialStride * sizeof(double);
+  const size_t need = part_bytes + ws.buf.size() * sizeof(double) + 64 * sizeof(double);
+  st = ensure_dev(s, need + 256);
+  if (st) return st;
+  double* dst = reinterpret_cast<double*>(static_cast<char*>(s->dev) + s->dev_cap) - 8;
+  st = run_walk(ws, 0, walk_steps(alg, m, n), magsum != nullptr, dst, stream);
+  if (st) return st;
+  PERM_CUDA_TRY(cudaMemcpyAsync(s->host, dst, 8 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  double re = s->host[0] + s->host[1], im = s->host[2] + s->host[3], mg = s->host[4];
+  normalize(alg, m, n, ws.scale_log2, &re, &im, &mg);
+  out[0] = re;
+  if (cplx) out[1] = im;
+  if (magsum) *magsum = mg;
+  return PERM_OK;
+}
+
+int walk_partial(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t k_begin,
+                 uint64_t k_end, int mag, double* partial, int partial_on_device, void* stream_) {
+  clear_error();
+  int st = check_shape(alg, m, n);
+  if (st) return st;
+  const uint64_t steps = walk_steps(alg, m, n);
+  if (k_begin > k_end || k_end > steps) {
+    set_error("Gray range outside the walk");
+    return PERM_BAD_ARG;
+  }
+  cudaStream_t stream = pick_stream(stream_);
+  HostMat A;
+  st = load_matrix(m, n, a, lda, dev_ptr, cplx, &A, stream);
+  if (st) return st;
+  WalkSetup ws;
+  st = build_walk(alg, A, &ws);
+  if (st) return st;
+  Scratch* s = scratch();
+  if (!s) return cuda_fail(cudaErrorNoDevice, "scratch");
+  const size_t part_bytes = (size_t)kMaxPartials * kPartialStride * sizeof(double);
+  st = ensure_dev(s, part_bytes + ws.buf.size() * sizeof(double) + 64 * sizeof(double) + 256);
+  if (st) return st;
+  if (k_begin == k_end) {  // empty shard
+    if (partial_on_device) {
+      PERM_CUDA_TRY(cudaMemsetAsync(partial, 0, 8 * sizeof(double), stream));
+    } else {
+      std::fill(partial, partial + 8, 0.0);
+    }
+    return PERM_OK;
+  }
+  double* dst = partial_on_device ? partial
+                                  : reinterpret_cast<double*>(static_cast<char*>(s->dev) + s->dev_cap) - 8;
+  st = run_walk(ws, k_begin, k_end, mag, dst, stream);
+  if (st) return st;
+  if (!partial_on_device) {
+    PERM_CUDA_TRY(cudaMemcpyAsync(s->host, dst, 8 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+    std::copy(s->host, s->host + 8, partial);
+  }
+  return PERM_OK;
+}
+
+int walk_finish(int alg, bool cplx, int m, int n, const double* a, int64_t lda, const double* partials, int G,
+                double* out, double* magsum) {
+  clear_error();
+  int st = check_shape(alg, m, n);
+  if (st) return st;
+  int s = 0;
+  if (alg == PERM_ALG_GLYNN && m < n) {
+    HostMat A;
+    st = load_matrix(m, n, a, lda, 0, cplx, &A, nullptr);
+    if (st) return st;
+    s = prescale_log2(A);
+  }
+  double h = 0, l = 0, h2 = 0, l2 = 0, mg = 0;
+  for (int g = 0; g < G; ++g) {
+    const double* p = partials + 8 * (size_t)g;
+    dd_add(h, l, p[0], p[1]);
+    dd_add(h2, l2, p[2], p[3]);
+    mg += p[4];
+  }
+  double re = h + l, im = h2 + l2;
+  normalize(alg, m, n, s, &re, &im, &mg);
+  out[0] = re;
+  if (cplx) out[1] = im;
+  if (magsum) *magsum = mg;
+  return PERM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int perm_version(void) { return 100; }
+const char* perm_last_error(void) { return permb200::last_error(); }
+
+int perm_set_device(int device) {
+  clear_error();
+  PERM_CUDA_TRY(cudaSetDevice(device));
+  return PERM_OK;
+}
+
+int perm_device_sm_count(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+int perm_glynn_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
+                   void* stream) {
+  return walk_single(PERM_ALG_GLYNN, false, m, n, a, lda, dev_ptr, out, magsum, stream);
+}
+int perm_glynn_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
+                    void* stream) {
+  return walk_single(PERM_ALG_GLYNN, true, m, n, a, lda, dev_ptr, out, magsum, stream);
+}
+int perm_ryser_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
+                   void* stream) {
+  return walk_single(PERM_ALG_RYSER, false, m, n, a, lda, dev_ptr, out, magsum, stream);
+}
+int perm_ryser_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
+                    void* stream) {
+  return walk_single(PERM_ALG_RYSER, true, m, n, a, lda, dev_ptr, out, magsum, stream);
+}
+
+uint64_t perm_walk_steps(int alg, int m, int n) {
+  if (check_shape(alg, m, n)) return 0;
+  return walk_steps(alg, m, n);
+}
+
+int perm_walk_shard(int alg, int m, int n, int rank, int world, uint64_t* k_begin, uint64_t* k_end) {
+  clear_error();
+  int st = check_shape(alg, m, n);
+  if (st) return st;
+  if (world < 1 || rank < 0 || rank >= world) {
+    set_error("bad rank/world");
+    return PERM_BAD_ARG;
+  }
+  const uint64_t steps = walk_steps(alg, m, n);
+  // split in units of 2^u with >= 64 units per rank where possible, so each
+  // shard boundary is aligned for the full-speed chunked kernel
+  int lg = 0;
+  while ((1 << lg) < world) ++lg;
+  const int lsteps = __builtin_ctzll(steps);
+  const int u = std::max(0, lsteps - lg - 6);
+  const uint64_t units = steps >> u;
+  const uint64_t b = (uint64_t)((unsigned __int128)units * (unsigned)rank / (unsigned)world);
+  const uint64_t e = (uint64_t)((unsigned __int128)units * (unsigned)(rank + 1) / (unsigned)world);
+  *k_begin = b << u;
+  *k_end = e << u;
+  return PERM_OK;
+}
+
+int perm_walk_partial_f64(int alg, int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t k_begin,
+                          uint64_t k_end, int mag, double* partial, int partial_on_device, void* stream) {
+  return walk_partial(alg, false, m, n, a, lda, dev_ptr, k_begin, k_end, mag, partial, partial_on_device, stream);
+}
+int perm_walk_partial_c128(int alg, int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t k_begin,
+                           uint64_t k_end, int mag, double* partial, int partial_on_device, void* stream) {
+  return walk_partial(alg, true, m, n, a, lda, dev_ptr, k_begin, k_end, mag, partial, partial_on_device, stream);
+}
+int perm_walk_finish_f64(int alg, int m, int n, const double* a, int64_t lda, const double* partials, int G,
+                         double* out, double* magsum) {
+  return walk_finish(alg, false, m, n, a, lda, partials, G, out, magsum);
+}
+int perm_walk_finish_c128(int alg, int m, int n, const double* a, int64_t lda, const double* partials, int G,
+                          double* out, double* magsum) {
+  return walk_finish(alg, true, m, n, a, lda, partials, G, out, magsum);
+}
+
+// src/dispatch.py:84-95 (strict '>' comparisons: ties take the else branch)
+int perm_select(int m, int n, const double* p, int64_t batch, int ngpu) {
+  (void)batch;
+  (void)ngpu;
+  if (m > n || m < 1) return -PERM_BAD_SHAPE;
+  const double r = (double)m / (double)n;
+  if ((double)n <= p[7]) {
+    if (m == n && (double)n <= p[3]) return PERM_ALG_COMBINATORIC;
+    const double h1 = p[0] * r + p[1] * n + p[2];
+    return h1 > 0 ? PERM_ALG_COMBINATORIC : PERM_ALG_GLYNN;
+  }
+  const double h2 = p[4] * r + p[5] * n + p[6];
+  return h2 > 0 ? PERM_ALG_GLYNN : PERM_ALG_RYSER;
+}
+
+}  // extern "C"

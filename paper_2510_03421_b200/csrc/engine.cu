@@ -1,0 +1,269 @@
+// Host-side engine internals: error state, scratch, matrix staging, walk
+// setup/normalization and the fixed-order finalize kernel.
+#include <algorithm>
+#include <cmath>
+
+#include "engine.cuh"
+
+namespace permb200 {
+
+// ---------------------------------------------------------------- errors
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+void clear_error() { g_err.clear(); }
+const char* last_error() { return g_err.c_str(); }
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string("CUDA error '") + cudaGetErrorString(e) + "' in " + what);
+  return PERM_CUDA;
+}
+
+// ---------------------------------------------------------------- scratch
+static thread_local Scratch g_scratch[16];
+
+Scratch* scratch() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (dev < 0 || dev >= 16) return nullptr;
+  Scratch* s = &g_scratch[dev];
+  if (s->device != dev) {
+    s->device = dev;
+    if (cudaMallocHost(&s->host, 64 * sizeof(double)) != cudaSuccess) return nullptr;
+  }
+  return s;
+}
+
+int ensure_dev(Scratch* s, size_t bytes) {
+  if (s->dev_cap >= bytes) return PERM_OK;
+  if (s->dev) {
+    PERM_CUDA_TRY(cudaDeviceSynchronize());
+    PERM_CUDA_TRY(cudaFree(s->dev));
+    s->dev = nullptr;
+    s->dev_cap = 0;
+  }
+  size_t cap = std::max<size_t>(bytes, 1 << 20);
+  PERM_CUDA_TRY(cudaMalloc(&s->dev, cap));
+  s->dev_cap = cap;
+  return PERM_OK;
+}
+
+cudaStream_t pick_stream(void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
+}
+
+// ---------------------------------------------------------------- matrices
+int load_matrix(int m, int n, const double* a, int64_t lda, int dev_ptr, bool cplx, HostMat* out,
+                cudaStream_t stream) {
+  if (m < 1 || n < 1) {
+    set_error("matrix must have m >= 1 and n >= 1");
+    return PERM_BAD_SHAPE;
+  }
+  if (lda < n) {
+    set_error("lda < n");
+    return PERM_BAD_ARG;
+  }
+  const int w = cplx ? 2 : 1;
+  out->m = m;
+  out->n = n;
+  out->cplx = cplx;
+  out->d.assign((size_t)m * n * w, 0.0);
+  if (dev_ptr) {
+    PERM_CUDA_TRY(cudaMemcpy2DAsync(out->d.data(), (size_t)n * w * sizeof(double), a,
+                                    (size_t)lda * w * sizeof(double), (size_t)n * w * sizeof(double), m,
+                                    cudaMemcpyDeviceToHost, stream));
+    PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  } else {
+    for (int i = 0; i < m; ++i)
+      std::memcpy(&out->d[(size_t)i * n * w], a + (size_t)i * lda * w, (size_t)n * w * sizeof(double));
+  }
+  return PERM_OK;
+}
+
+// ---------------------------------------------------------------- setup
+uint64_t walk_steps(int alg, int m, int n) {
+  (void)m;
+  if (alg == PERM_ALG_GLYNN) return 1ull << (n - 1);
+  return (n >= 64) ? 0 : (1ull << n);
+}
+
+int prescale_log2(const HostMat& A) {
+  long double ss = 0;
+  for (int i = 0; i < A.m; ++i)
+    for (int j = 0; j < A.n; ++j) {
+      long double r = A.re(i, j), im = A.im(i, j);
+      ss += r * r + im * im;
+    }
+  double rms = std::sqrt((double)(ss / ((long double)A.m * A.n)));
+  if (!std::isfinite(rms) || rms == 0.0) return 0;
+  // round half away from zero, as Python's round() differs only on exact .5
+  double e = -std::log2(rms);
+  double r = std::nearbyint(e);  // ties-to-even, same as Python round()
+  return (int)r;
+}
+
+static inline double binom_d(int a, int b) {
+  if (b < 0 || b > a) return 0.0;
+  unsigned __int128 r = 1;
+  for (int i = 1; i <= b; ++i) r = r * (unsigned __int128)(a - b + i) / (unsigned __int128)i;
+  return (double)(long double)r;
+}
+
+int build_walk(int alg, const HostMat& A, WalkSetup* ws) {
+  const int m = A.m, n = A.n;
+  const int w = A.cplx ? 2 : 1;
+  ws->cplx = A.cplx;
+  ws->scale_log2 = 0;
+  ws->weighted = false;
+  ws->wlen = 0;
+  if (alg == PERM_ALG_GLYNN) {
+    // ones-padded n x n matrix, real rows scaled by k = 2^s
+    const int s = (m < n) ? prescale_log2(A) : 0;
+    ws->scale_log2 = s;
+    ws->P = n;
+    ws->B = n - 1;
+    ws->v0_off = 0;
+    ws->U_off = (size_t)n * w;
+    ws->buf.assign((size_t)n * w + (size_t)(n - 1) * n * w, 0.0);
+    auto row_re = [&](int i, int j) { return i < m ? std::ldexp(A.re(i, j), s) : 1.0; };
+    auto row_im = [&](int i, int j) { return i < m ? std::ldexp(A.im(i, j), s) : 0.0; };
+    for (int j = 0; j < n; ++j) {
+      // exactly-rounded column sums (long double accumulation)
+      long double sr = 0, si = 0;
+      for (int i = 0; i < n; ++i) { sr += row_re(i, j); si += row_im(i, j); }
+      ws->buf[(size_t)j * w] = (double)sr;
+      if (w == 2) ws->buf[(size_t)j * w + 1] = (double)si;
+    }
+    for (int t = 0; t < n - 1; ++t) {
+      const int i = n - 1 - t;  // Gray bit t flips row n-1-t (src/_kernels.py:393)
+      for (int j = 0; j < n; ++j) {
+        ws->buf[ws->U_off + ((size_t)t * n + j) * w] = -2.0 * row_re(i, j);
+        if (w == 2) ws->buf[ws->U_off + ((size_t)t * n + j) * w + 1] = -2.0 * row_im(i, j);
+      }
+    }
+    return PERM_OK;
+  }
+  if (alg == PERM_ALG_RYSER) {
+    // state = row sums over the chosen column subset; Gray bit t = column t
+    ws->P = m;
+    ws->B = n;
+    ws->v0_off = 0;
+    ws->U_off = (size_t)m * w;
+    size_t nU = (size_t)n * m * w;
+    if (m < n) {
+      ws->weighted = true;
+      ws->wlen = n + 1;
+    }
+    ws->w_off = ws->U_off + nU;
+    ws->buf.assign(ws->w_off + ws->wlen, 0.0);
+    for (int t = 0; t < n; ++t)
+      for (int i = 0; i < m; ++i) {
+        ws->buf[ws->U_off + ((size_t)t * m + i) * w] = A.re(i, t);
+        if (w == 2) ws->buf[ws->U_off + ((size_t)t * m + i) * w + 1] = A.im(i, t);
+      }
+    if (ws->weighted)  // src/algorithms.py:110-115; zero above size m
+      for (int s = 1; s <= m; ++s) {
+        double c = binom_d(n - s, m - s);
+        ws->buf[ws->w_off + s] = ((m - s) & 1) ? -c : c;
+      }
+    return PERM_OK;
+  }
+  set_error("unknown algorithm");
+  return PERM_BAD_ARG;
+}
+
+void normalize(int alg, int m, int n, int scale_log2, double* re, double* im, double* mag) {
+  if (alg == PERM_ALG_GLYNN) {
+    // per = sum / (2^(n-1) * (n-m)! * k^m)   (src/algorithms.py:159-160, 182-184)
+    const int e = -(n - 1) - m * scale_log2;
+    double f = 1.0;
+    for (int i = 2; i <= n - m; ++i) f *= (double)i;
+    *re = std::ldexp(*re, e) / f;
+    *im = std::ldexp(*im, e) / f;
+    *mag = std::ldexp(*mag, e) / f;
+  } else if (alg == PERM_ALG_RYSER) {
+    if (m == n && (n & 1)) {  // src/_kernels.py:143-144
+      *re = -*re;
+      *im = -*im;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void walk_finalize_kernel(const double* __restrict__ partials, int nparts, double* __restrict__ out) {
+  __shared__ double red[256][5];
+  const int tid = threadIdx.x;
+  double h = 0, l = 0, h2 = 0, l2 = 0, mg = 0;
+  for (int i = tid; i < nparts; i += blockDim.x) {
+    const double* p = partials + (size_t)i * kPartialStride;
+    dd_add(h, l, p[0], p[1]);
+    dd_add(h2, l2, p[2], p[3]);
+    mg += p[4];
+  }
+  red[tid][0] = h; red[tid][1] = l; red[tid][2] = h2; red[tid][3] = l2; red[tid][4] = mg;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (tid < s) {
+      dd_add(red[tid][0], red[tid][1], red[tid + s][0], red[tid + s][1]);
+      dd_add(red[tid][2], red[tid][3], red[tid + s][2], red[tid + s][3]);
+      red[tid][4] += red[tid + s][4];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    out[0] = red[0][0]; out[1] = red[0][1]; out[2] = red[0][2]; out[3] = red[0][3]; out[4] = red[0][4];
+    out[5] = 0.0; out[6] = 0.0; out[7] = 0.0;
+  }
+}
+
+walk_fn walk_lookup_f64_w0(int P);
+walk_fn walk_lookup_f64_w1(int P);
+walk_fn walk_lookup_c128_w0(int P);
+walk_fn walk_lookup_c128_w1(int P);
+
+walk_fn walk_lookup(int dtype, bool weighted, int P) {
+  if (dtype == 0) return weighted ? walk_lookup_f64_w1(P) : walk_lookup_f64_w0(P);
+  return weighted ? walk_lookup_c128_w1(P) : walk_lookup_c128_w0(P);
+}
+
+int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst, cudaStream_t stream) {
+  if (ws.P < 1 || ws.P > 64) {
+    set_error("state length out of range (1..64)");
+    return PERM_BAD_SHAPE;
+  }
+  Scratch* s = scratch();
+  if (!s) {
+    set_error("no CUDA device");
+    return PERM_CUDA;
+  }
+  const size_t part_bytes = (size_t)kMaxPartials * kPartialStride * sizeof(double);
+  const size_t data_bytes = ws.buf.size() * sizeof(double);
+  int st = ensure_dev(s, part_bytes + data_bytes + 256);
+  if (st) return st;
+  double* partials = static_cast<double*>(s->dev);
+  double* data = partials + (size_t)kMaxPartials * kPartialStride;
+  PERM_CUDA_TRY(cudaMemcpyAsync(data, ws.buf.data(), data_bytes, cudaMemcpyHostToDevice, stream));
+  walk_fn fn = walk_lookup(ws.cplx ? 1 : 0, ws.weighted, ws.P);
+  if (!fn) {
+    set_error("no walk kernel for this state length");
+    return PERM_BAD_SHAPE;
+  }
+  WalkJob job;
+  job.dtype = ws.cplx ? 1 : 0;
+  job.P = ws.P;
+  job.B = ws.B;
+  job.weighted = ws.weighted;
+  job.v0 = data + ws.v0_off;
+  job.U = data + ws.U_off;
+  job.w = ws.weighted ? data + ws.w_off : nullptr;
+  job.wlen = ws.wlen;
+  job.mag = mag;
+  job.k_begin = k_begin;
+  job.k_end = k_end;
+  job.partials = partials;
+  WalkPlan plan;
+  PERM_CUDA_TRY(fn(job, &plan, stream));
+  walk_finalize_kernel<<<1, 256, 0, stream>>>(partials, plan.grid, dst);
+  PERM_CUDA_TRY(cudaGetLastError());
+  return PERM_OK;
+}
+
+}  // namespace permb200

@@ -1,0 +1,72 @@
+// Host-side engine internals shared by the C-ABI translation units:
+// error state, per-thread device scratch, matrix staging, walk setup.
+#pragma once
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/permanent_b200.h"
+#include "walk_launch.cuh"
+
+namespace permb200 {
+
+// ---- errors --------------------------------------------------------------
+void set_error(const std::string& msg);
+void clear_error();
+int cuda_fail(cudaError_t e, const char* what);
+
+#define PERM_CUDA_TRY(expr)                                      \
+  do {                                                           \
+    cudaError_t _e = (expr);                                     \
+    if (_e != cudaSuccess) return ::permb200::cuda_fail(_e, #expr); \
+  } while (0)
+
+// ---- per-(thread, device) scratch ----------------------------------------
+struct Scratch {
+  int device = -1;
+  void* dev = nullptr;       // device scratch
+  size_t dev_cap = 0;
+  double* host = nullptr;    // pinned host result buffer (64 doubles)
+  cudaStream_t own = nullptr;
+};
+Scratch* scratch();                              // for the current device
+int ensure_dev(Scratch* s, size_t bytes);        // grow device scratch
+cudaStream_t pick_stream(void* stream);
+
+// ---- matrices --------------------------------------------------------------
+// A dense row-major copy in host memory (doubles; complex interleaved).
+struct HostMat {
+  int m = 0, n = 0;
+  bool cplx = false;
+  std::vector<double> d;  // m*n*(cplx?2:1)
+  double re(int i, int j) const { return cplx ? d[2 * ((size_t)i * n + j)] : d[(size_t)i * n + j]; }
+  double im(int i, int j) const { return cplx ? d[2 * ((size_t)i * n + j) + 1] : 0.0; }
+};
+int load_matrix(int m, int n, const double* a, int64_t lda, int dev_ptr, bool cplx, HostMat* out,
+                cudaStream_t stream);
+
+// ---- walk setup --------------------------------------
+struct WalkSetup {
+  int P = 0, B = 0;
+  bool weighted = false;
+  bool cplx = false;
+  int scale_log2 = 0;                // Glynn rectangular pre-scale k = 2^scale_log2
+  std::vector<double> buf;           // v0 [P], U [B][P] (complex interleaved), then w [n+1]
+  size_t v0_off = 0, U_off = 0, w_off = 0;  // offsets in doubles
+  int wlen = 0;
+};
+int build_walk(int alg, const HostMat& A, WalkSetup* ws);
+// Power-of-two pre-scale exponent for rectangular Glynn: round(-log2(RMS|a|)).
+int prescale_log2(const HostMat& A);
+// Normalize a raw walk sum (re, im, mag) into the permanent.
+void normalize(int alg, int m, int n, int scale_log2, double* re, double* im, double* mag);
+// Run the walk over [k_begin, k_end) -> 8 raw doubles at `dst` (device).
+int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst, cudaStream_t stream);
+
+uint64_t walk_steps(int alg, int m, int n);
+
+}  // namespace permb200

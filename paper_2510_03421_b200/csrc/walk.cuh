@@ -1,0 +1,346 @@
+// Gray-code walk engine: the FP64 / complex128 Glynn and Ryser kernels.
+//
+// One template covers every floating-point enumeration kernel of the
+// reference (src/_kernels.py = /root/reference/pkg/src/permanent/_kernels.py):
+//
+//   Glynn square      glynn_sq    :373-409   P = n, B = n-1, v0 = column sums,
+//                                            U[t] = -2 * row(n-1-t), term (-1)^k
+//   Glynn rectangular glynn_rect  :531-577   same on the ones-padded n x n matrix
+//                                            (real rows pre-scaled by a power of two)
+//   Ryser square      ryser_sq    :115-145   P = n, B = n, v0 = 0, U[t] = column t,
+//                                            term (-1)^k, per = (-1)^n * sum
+//   Ryser rectangular ryser_rect  :226-262   P = m, B = n, all 2^n subsets, term
+//                                            w[popcount(gray(k))] * prod
+//
+// State after Gray index k: v = v0 + sum_{t : bit t of gray(k)} U[t]; step k
+// flips Gray bit t = ctz(k) (v += U[t] if the bit becomes set, else -=).
+//
+// Work decomposition.  The index space [k_begin, k_begin+steps)
+// is cut into chunks of L = 2^r consecutive indices; lane `l` of warp-group g
+// owns chunk 32*g + l, so the 32 chunks of a warp are adjacent.  Inside a
+// chunk every lane performs the *same* flip schedule (Gray bit ctz(local
+// index), same direction) -- the only lane-dependent step is local index L/2,
+// whose direction is bit 0 of the chunk number -- so every U[t] read is a
+// warp-uniform shared-memory broadcast and the steps are unrolled by 8 with
+// compile-time flip rows t = 0, 1, 0, 2, 0, 1, 0.  Seeding a chunk costs
+// ~B/64 column sums per lane (warp-cooperative) plus <= 6 row FMAs.
+//
+// Accumulation: a plain FP64 sum over each chunk (<= L terms), folded into a
+// per-thread double-double with two_sum; double-double warp-shuffle and block
+// reductions; one partial (hi, lo) per block, combined in fixed order by
+// walk_finalize_kernel -> deterministic for a given launch shape.
+#pragma once
+#include "common.cuh"
+
+namespace permb200 {
+
+constexpr int kWalkThreads = 256;
+constexpr int kWalkWarps = kWalkThreads / 32;
+constexpr int kPartialStride = 8;  // doubles per block partial: hi, lo, im_hi, im_lo, mag, -, -, -
+
+struct WalkArgs {
+  const void* v0;        // [P] T
+  const void* U;         // [B][P] T
+  const double* w;       // [wlen] popcount weights (weighted walks only)
+  int B;                 // Gray bits
+  int log2L;             // chunk length exponent (>= 3)
+  int wlen;              // number of weights
+  int mag;               // also accumulate sum |term| (metric (ii) scale)
+  uint64_t k_begin;      // first Gray index, multiple of 32*L
+  uint64_t ngroups;      // number of 32-chunk groups
+  double* partials;      // [gridDim.x][kPartialStride]
+};
+
+// Shared-memory reads of U rows are volatile on purpose: with plain loads
+// ptxas hoists every row read of the 8 unrolled steps to the top of the block
+// (the rows are loop-invariant), keeping ~8 rows live and spilling at P >= 20.
+// A warp-uniform read is a single broadcast wavefront, so re-reading is cheap.
+template <typename T>
+__device__ __forceinline__ T ld_row(const T* row, int j) {
+  if constexpr (sizeof(T) == 16) {
+    const volatile double2* p = reinterpret_cast<const volatile double2*>(row) + j;
+    double2 u;
+    u.x = p->x;
+    u.y = p->y;
+    return cd_make(u.x, u.y);
+  } else {
+    return reinterpret_cast<const volatile double*>(row)[j];
+  }
+}
+
+template <typename T, int P>
+__device__ __forceinline__ void row_add(T (&v)[P], const T* __restrict__ row) {
+  if constexpr (sizeof(T) == 8 && P >= 2) {
+    const volatile double2* r2 = reinterpret_cast<const volatile double2*>(row);
+#pragma unroll
+    for (int j = 0; j < P / 2; ++j) {
+      double2 u; u.x = r2[j].x; u.y = r2[j].y;
+      v[2 * j] = Num<T>::add(v[2 * j], u.x);
+      v[2 * j + 1] = Num<T>::add(v[2 * j + 1], u.y);
+    }
+    if constexpr (P & 1) v[P - 1] = Num<T>::add(v[P - 1], ld_row<T>(row, P - 1));
+  } else {
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = Num<T>::add(v[j], ld_row<T>(row, j));
+  }
+}
+
+template <typename T, int P>
+__device__ __forceinline__ void row_sub(T (&v)[P], const T* __restrict__ row) {
+  if constexpr (sizeof(T) == 8 && P >= 2) {
+    const volatile double2* r2 = reinterpret_cast<const volatile double2*>(row);
+#pragma unroll
+    for (int j = 0; j < P / 2; ++j) {
+      double2 u; u.x = r2[j].x; u.y = r2[j].y;
+      v[2 * j] = Num<T>::sub(v[2 * j], u.x);
+      v[2 * j + 1] = Num<T>::sub(v[2 * j + 1], u.y);
+    }
+    if constexpr (P & 1) v[P - 1] = Num<T>::sub(v[P - 1], ld_row<T>(row, P - 1));
+  } else {
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = Num<T>::sub(v[j], ld_row<T>(row, j));
+  }
+}
+
+template <typename T, int P>
+__device__ __forceinline__ void row_fma(T (&v)[P], double s, const T* __restrict__ row) {
+  if constexpr (sizeof(T) == 8 && P >= 2) {
+    const volatile double2* r2 = reinterpret_cast<const volatile double2*>(row);
+#pragma unroll
+    for (int j = 0; j < P / 2; ++j) {
+      double2 u; u.x = r2[j].x; u.y = r2[j].y;
+      v[2 * j] = Num<T>::fmas(s, u.x, v[2 * j]);
+      v[2 * j + 1] = Num<T>::fmas(s, u.y, v[2 * j + 1]);
+    }
+    if constexpr (P & 1) v[P - 1] = Num<T>::fmas(s, ld_row<T>(row, P - 1), v[P - 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = Num<T>::fmas(s, ld_row<T>(row, j), v[j]);
+  }
+}
+
+// Row stride (elements) of U in shared memory: even for doubles so a row
+// starts 16-byte aligned and can be read with LDS.128.
+template <typename T, int P>
+__host__ __device__ constexpr int row_stride() { return (sizeof(T) == 8) ? ((P + 1) & ~1) : P; }
+
+// Product of the state vector with kChains interleaved multiply chains: depth
+// P/kChains, only kChains temporaries live (a full pairwise tree keeps P/2
+// extra values live and spills at P >= 20).
+constexpr int kChains = 4;
+template <typename T, int P>
+__device__ __forceinline__ T chain_product(const T (&v)[P]) {
+  constexpr int C = (P < kChains) ? P : kChains;
+  T c[C];
+#pragma unroll
+  for (int i = 0; i < C; ++i) c[i] = v[i];
+#pragma unroll
+  for (int j = C; j < P; ++j) c[j % C] = Num<T>::mul(c[j % C], v[j]);
+  if constexpr (C == 1) return c[0];
+  else if constexpr (C == 2) return Num<T>::mul(c[0], c[1]);
+  else if constexpr (C == 3) return Num<T>::mul(Num<T>::mul(c[0], c[1]), c[2]);
+  else return Num<T>::mul(Num<T>::mul(c[0], c[1]), Num<T>::mul(c[2], c[3]));
+}
+
+// Occupancy target: cap registers so at least 16 warps per SM stay resident
+// where the state vector fits (FP64-pipe bound code needs ILP x warps, not
+// maximal occupancy); large complex vectors get the whole register file.
+template <typename T, int P>
+__host__ __device__ constexpr int walk_min_blocks() {
+  return (Num<T>::kDoubles == 1) ? ((P <= 20) ? 3 : (P <= 44) ? 2 : 1) : ((P <= 14) ? 2 : 1);
+}
+
+template <typename T, int P, bool W>
+struct Term {
+  // chunk sum, magnitude sum
+  __device__ __forceinline__ static void add(const T (&v)[P], int sign, int pc, const double* sW, T& acc,
+                                             double& mag, int mag_on) {
+    T p = chain_product<T, P>(v);
+    if constexpr (W) {
+      double wt = sW[pc];
+      acc = Num<T>::add(acc, Num<T>::scale(wt, p));
+      if (mag_on) mag += fabs(wt) * Num<T>::absval(p);
+    } else {
+      acc = (sign > 0) ? Num<T>::add(acc, p) : Num<T>::sub(acc, p);
+      if (mag_on) mag += Num<T>::absval(p);
+    }
+  }
+};
+
+template <typename T, int P, bool W>
+__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_kernel(WalkArgs args) {
+  constexpr int PS = row_stride<T, P>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sU = reinterpret_cast<T*>(smem_raw);        // [B][PS]
+  T* sV0 = sU + (size_t)args.B * PS;              // [PS]
+  T* sWarp = sV0 + PS;                            // [kWalkWarps][PS]
+  double* sW = reinterpret_cast<double*>(sWarp + kWalkWarps * PS);  // [wlen]
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int B = args.B;
+  {
+    const T* gU = static_cast<const T*>(args.U);
+    const T* gV0 = static_cast<const T*>(args.v0);
+    for (int i = tid; i < B * P; i += kWalkThreads) sU[(i / P) * PS + (i % P)] = gU[i];
+    for (int j = tid; j < P; j += kWalkThreads) sV0[j] = gV0[j];
+    if constexpr (W)
+      for (int i = tid; i < args.wlen; i += kWalkThreads) sW[i] = args.w[i];
+  }
+  __syncthreads();
+
+  const int log2L = args.log2L;
+  const uint64_t L = 1ull << log2L;
+  const uint64_t nq = L >> 3;
+  const uint64_t bmask = (B >= 64) ? ~0ull : ((1ull << B) - 1);
+  const uint64_t hmask = (~0ull << (log2L + 5)) & bmask;  // warp-uniform Gray bits
+  const int mag_on = args.mag;
+  T* myWarp = sWarp + warp * PS;
+
+  double hi = 0.0, lo = 0.0, hi_i = 0.0, lo_i = 0.0, mag = 0.0;
+  const uint64_t total_warps = (uint64_t)gridDim.x * kWalkWarps;
+
+  for (uint64_t g = (uint64_t)blockIdx.x * kWalkWarps + warp; g < args.ngroups; g += total_warps) {
+    const uint64_t kb = args.k_begin + ((g * 32) << log2L);
+    const uint64_t k0 = kb + ((uint64_t)lane << log2L);
+    // ---- warp-cooperative seed of the bits shared by the 32 chunks
+    {
+      const uint64_t gb = (kb ^ (kb >> 1)) & hmask;
+      for (int j = lane; j < P; j += 32) {
+        T acc = sV0[j];
+        uint64_t bits = gb;
+        while (bits) {
+          int t = __ffsll((long long)bits) - 1;
+          bits &= bits - 1;
+          acc = Num<T>::add(acc, sU[t * PS + j]);
+        }
+        myWarp[j] = acc;
+      }
+    }
+    __syncwarp();
+    T v[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = myWarp[j];
+    __syncwarp();
+    const uint64_t g0 = k0 ^ (k0 >> 1);
+    // ---- lane-dependent Gray bits: positions log2L-1 .. log2L+4
+#pragma unroll
+    for (int d = -1; d <= 4; ++d) {
+      const int b = log2L + d;
+      if (b < B) {
+        const double s = (double)((g0 >> b) & 1);
+        row_fma<T, P>(v, s, sU + b * PS);
+      }
+    }
+    int pc = __popcll(g0);
+
+    T acc = Num<T>::zero();
+    for (uint64_t q = 0; q < nq; ++q) {
+      const uint64_t l0 = q << 3;
+      if (q) {
+        const int t = __ffsll((long long)l0) - 1;
+        const uint64_t k = k0 + l0;
+        const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
+        row_fma<T, P>(v, set ? 1.0 : -1.0, sU + t * PS);
+        if constexpr (W) pc += set ? 1 : -1;
+      }
+      Term<T, P, W>::add(v, +1, pc, sW, acc, mag, mag_on);
+      row_add<T, P>(v, sU);  // l = 1: bit 0 set
+      if constexpr (W) ++pc;
+      Term<T, P, W>::add(v, -1, pc, sW, acc, mag, mag_on);
+      row_add<T, P>(v, sU + PS);  // l = 2: bit 1 set
+      if constexpr (W) ++pc;
+      Term<T, P, W>::add(v, +1, pc, sW, acc, mag, mag_on);
+      row_sub<T, P>(v, sU);  // l = 3: bit 0 cleared
+      if constexpr (W) --pc;
+      Term<T, P, W>::add(v, -1, pc, sW, acc, mag, mag_on);
+      {  // l = 4: bit 2 toggles; set iff bit 3 of (k0 + l0) is clear
+        const int b3 = (int)(((k0 + l0) >> 3) & 1);
+        row_fma<T, P>(v, b3 ? -1.0 : 1.0, sU + 2 * PS);
+        if constexpr (W) pc += b3 ? -1 : 1;
+      }
+      Term<T, P, W>::add(v, +1, pc, sW, acc, mag, mag_on);
+      row_add<T, P>(v, sU);  // l = 5: bit 0 set
+      if constexpr (W) ++pc;
+      Term<T, P, W>::add(v, -1, pc, sW, acc, mag, mag_on);
+      row_sub<T, P>(v, sU + PS);  // l = 6: bit 1 cleared
+      if constexpr (W) --pc;
+      Term<T, P, W>::add(v, +1, pc, sW, acc, mag, mag_on);
+      row_sub<T, P>(v, sU);  // l = 7: bit 0 cleared
+      if constexpr (W) --pc;
+      Term<T, P, W>::add(v, -1, pc, sW, acc, mag, mag_on);
+    }
+    dd_acc(hi, lo, Num<T>::re(acc));
+    if constexpr (sizeof(T) == 16) dd_acc(hi_i, lo_i, Num<T>::im(acc));
+  }
+
+  // ---- deterministic reduction: warp shuffle, then warp 0 over the block
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    double h2 = __shfl_down_sync(0xffffffffu, hi, off), l2 = __shfl_down_sync(0xffffffffu, lo, off);
+    dd_add(hi, lo, h2, l2);
+    if constexpr (sizeof(T) == 16) {
+      double h3 = __shfl_down_sync(0xffffffffu, hi_i, off), l3 = __shfl_down_sync(0xffffffffu, lo_i, off);
+      dd_add(hi_i, lo_i, h3, l3);
+    }
+    mag += __shfl_down_sync(0xffffffffu, mag, off);
+  }
+  __shared__ double red[kWalkWarps][5];
+  if (lane == 0) {
+    red[warp][0] = hi; red[warp][1] = lo; red[warp][2] = hi_i; red[warp][3] = lo_i; red[warp][4] = mag;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double H = red[0][0], Lo = red[0][1], Hi2 = red[0][2], Lo2 = red[0][3], M = red[0][4];
+    for (int w = 1; w < kWalkWarps; ++w) {
+      dd_add(H, Lo, red[w][0], red[w][1]);
+      dd_add(Hi2, Lo2, red[w][2], red[w][3]);
+      M += red[w][4];
+    }
+    double* out = args.partials + (size_t)blockIdx.x * kPartialStride;
+    out[0] = H; out[1] = Lo; out[2] = Hi2; out[3] = Lo2; out[4] = M;
+  }
+}
+
+// Single-thread walk for tiny index spaces (< 32 chunks of 8): runtime P.
+// Same arithmetic as walk_kernel (plain sum per 'chunk' of the whole range).
+template <typename T>
+__global__ void walk_small_kernel(const T* __restrict__ v0, const T* __restrict__ U, const double* __restrict__ w,
+                                  int P, int B, int weighted, int mag_on, uint64_t k_begin, uint64_t k_end,
+                                  double* partials) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  T v[64];
+  const uint64_t g0 = k_begin ^ (k_begin >> 1);
+  for (int j = 0; j < P; ++j) v[j] = v0[j];
+  for (int t = 0; t < B; ++t)
+    if ((g0 >> t) & 1)
+      for (int j = 0; j < P; ++j) v[j] = Num<T>::add(v[j], U[t * P + j]);
+  int pc = __popcll(g0);
+  T acc = Num<T>::zero();
+  double mag = 0.0;
+  for (uint64_t k = k_begin; k < k_end; ++k) {
+    if (k != k_begin) {
+      const int t = __ffsll((long long)k) - 1;
+      const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
+      for (int j = 0; j < P; ++j) v[j] = set ? Num<T>::add(v[j], U[t * P + j]) : Num<T>::sub(v[j], U[t * P + j]);
+      pc += set ? 1 : -1;
+    }
+    T p = v[0];
+    for (int j = 1; j < P; ++j) p = Num<T>::mul(p, v[j]);
+    if (weighted) {
+      acc = Num<T>::add(acc, Num<T>::scale(w[pc], p));
+      if (mag_on) mag += fabs(w[pc]) * Num<T>::absval(p);
+    } else {
+      acc = (k & 1) ? Num<T>::sub(acc, p) : Num<T>::add(acc, p);
+      if (mag_on) mag += Num<T>::absval(p);
+    }
+  }
+  partials[0] = Num<T>::re(acc); partials[1] = 0.0;
+  partials[2] = Num<T>::im(acc); partials[3] = 0.0;
+  partials[4] = mag;
+}
+
+// Fixed-order combine of block partials -> out[0..4] (one block).
+__global__ void walk_finalize_kernel(const double* __restrict__ partials, int nparts, double* __restrict__ out);
+
+}  // namespace permb200

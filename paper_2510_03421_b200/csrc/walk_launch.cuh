@@ -1,0 +1,107 @@
+// Host-side planning and launch of the Gray-walk kernels.
+#pragma once
+#include <utility>
+
+#include "walk.cuh"
+
+namespace permb200 {
+
+struct WalkJob {
+  int dtype;             // 0 = f64, 1 = c128
+  int P, B;
+  bool weighted;
+  const void* v0;        // device
+  const void* U;         // device
+  const double* w;       // device (weighted) or null
+  int wlen;
+  int mag;
+  uint64_t k_begin, k_end;  // Gray range; k_begin, k_end multiples of 32*L (or tiny range)
+  double* partials;      // device scratch, >= max_partials() * kPartialStride doubles
+};
+
+struct WalkPlan {
+  int grid = 0;          // number of block partials written
+  int log2L = 0;
+  uint64_t ngroups = 0;
+  bool small = false;
+};
+
+using walk_fn = cudaError_t (*)(const WalkJob&, WalkPlan*, cudaStream_t);
+
+// Upper bound on block partials any plan writes (grid <= 148 * 8).
+constexpr int kMaxPartials = 148 * 16;
+
+// Chunk length for a range of `steps` Gray indices over `lanes` threads:
+// long chunks amortize seeding (~6 row FMAs + B/64 sums per chunk), many
+// chunks per lane bound the tail of the static lane->chunk assignment.
+inline int choose_log2L(uint64_t steps, uint64_t lanes) {
+  int r = 3;
+  // grow L while every lane still gets >= 24 chunks and L <= 2^14
+  while (r < 14 && (steps >> (r + 1)) >= 24 * lanes) ++r;
+  // need at least 32 chunks (one warp-group)
+  while (r > 3 && (steps >> r) < 32) --r;
+  return r;
+}
+
+// Largest power-of-two alignment that divides x (x != 0), capped.
+inline int align_log2(uint64_t x) { return x ? __builtin_ctzll(x) : 64; }
+
+template <typename T, int P, bool W>
+cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream) {
+  constexpr int PS = row_stride<T, P>();
+  const uint64_t steps = job.k_end - job.k_begin;
+  const size_t smem = (size_t)(job.B * PS + PS + kWalkWarps * PS) * sizeof(T) + (size_t)(W ? job.wlen : 0) * 8;
+  auto kern = walk_kernel<T, P, W>;
+  static int attr_smem = 0;  // benign race: idempotent
+  if ((int)smem > 48 * 1024 && attr_smem < (int)smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_smem = (int)smem;
+  }
+  int dev = 0, nsm = 148, bps = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kWalkThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (bps < 1) bps = 1;
+  if (bps * nsm > kMaxPartials) bps = kMaxPartials / nsm;
+  const uint64_t lanes = (uint64_t)bps * nsm * kWalkThreads;
+  // alignment: chunks of L must tile [k_begin, k_end) in groups of 32
+  int r = choose_log2L(steps, lanes);
+  const int amax = std::min(align_log2(job.k_begin), align_log2(steps)) - 5;
+  if (r > amax) r = amax;
+  if (r < 3 || (steps >> r) < 32) {
+    plan->small = true;
+    plan->grid = 1;
+    plan->log2L = 0;
+    walk_small_kernel<T><<<1, 32, 0, stream>>>(static_cast<const T*>(job.v0), static_cast<const T*>(job.U), job.w,
+                                               P, job.B, W ? 1 : 0, job.mag, job.k_begin, job.k_end, job.partials);
+    return cudaGetLastError();
+  }
+  WalkArgs a;
+  a.v0 = job.v0; a.U = job.U; a.w = job.w; a.B = job.B; a.log2L = r; a.wlen = job.wlen; a.mag = job.mag;
+  a.k_begin = job.k_begin;
+  a.ngroups = (steps >> r) / 32;
+  a.partials = job.partials;
+  uint64_t grid = (uint64_t)bps * nsm;
+  const uint64_t need = (a.ngroups + kWalkWarps - 1) / kWalkWarps;
+  if (grid > need) grid = need;
+  plan->small = false;
+  plan->grid = (int)grid;
+  plan->log2L = r;
+  plan->ngroups = a.ngroups;
+  kern<<<(unsigned)grid, kWalkThreads, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T, bool W, int... Ps>
+walk_fn walk_pick(int P, std::integer_sequence<int, Ps...>) {
+  walk_fn fn = nullptr;
+  ((P == Ps + 1 ? (fn = &launch_walk<T, Ps + 1, W>, 0) : 0), ...);
+  return fn;
+}
+
+// Per-translation-unit lookup tables (instantiated in walk_inst_*.cu).
+walk_fn walk_lookup(int dtype, bool weighted, int P);
+
+}  // namespace permb200
