@@ -72,6 +72,32 @@ int perm_ryser_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, doub
 int perm_ryser_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
                     void* stream);
 
+/* ---- combinatoric (src/_kernels.py:28-56, 59-108; src/algorithms.py:71-90)
+ * Depth-first enumeration of the m-permutations with prefix products and
+ * zero pruning, the DFS tree split at a prefix depth across threads.
+ * PERM_BUDGET when P(n, m) > step_budget (StepBudgetExceeded). */
+int perm_comb_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t step_budget, double* out,
+                  void* stream);
+int perm_comb_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t step_budget, double* out,
+                   void* stream);
+int perm_comb_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, uint64_t step_budget, int64_t* out,
+                  void* stream);
+
+/* ---- exact integer path (north_star item 3) -----------------------------
+ * width = 64: the reference's checked-int64 semantics bit for bit
+ *   (glynn_sq_int / glynn_rect_int / ryser_sq_int / ryser_rect_int,
+ *   src/_kernels.py:148-365, 412-697, and the exact-division checks of
+ *   src/algorithms.py:431-461): PERM_OVERFLOW exactly when the reference
+ *   reports overflowed=True (its OverflowError, src/__init__.py:43-47).
+ * width = 128: exact permanent via a mod-2^128 walk, certified to fit by an
+ *   FP64 run and its magnitude-sum error bound; PERM_OVERFLOW if the
+ *   certificate fails.
+ * out[0], out[1] = low, high 64 bits (two's complement); *fits_int64 set. */
+int perm_glynn_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, int64_t* out,
+                   int* fits_int64, void* stream);
+int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, int64_t* out,
+                   int* fits_int64, void* stream);
+
 /* ---- sharded walks (one Gray range per GPU / rank) --------
  * perm_walk_steps: length of the Gray index space of (alg, m, n): 2^(n-1)
  * for Glynn, 2^n for Ryser.  perm_walk_shard: the [k_begin, k_end) of

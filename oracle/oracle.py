@@ -126,7 +126,7 @@ def _plain(value, kind):
     return float(value) if kind == "f64" else complex(value)
 
 
-def permanent(alg: str, a, step_budget: int = 2_000_000_000):
+def permanent(alg: str, a, step_budget: int = 2_000_000_000, compiled=None):
     """(value, overflowed) exactly as ``run_algorithm`` (src/algorithms.py:187-201)
     returns it, for an m <= n matrix."""
     a = as_array(a)
@@ -171,9 +171,20 @@ def permanent(alg: str, a, step_budget: int = 2_000_000_000):
         acc = kernel("glynn_rect", a)
         if kind == "f64":
             acc = np.float64(acc)
+        elif _compiled(1 << (n - 1), compiled):
+            # numba hands back a Python complex, whose division by a float
+            # is componentwise true division; the interpreted kernel's numpy
+            # complex128 divides by multiplying with the reciprocal -- the two
+            # modes differ in the last bit here (src/algorithms.py:462-463)
+            acc = complex(acc)
         value = acc / (2.0 ** (n - 1)) / float(math.factorial(n - m))
         return _plain(value, kind), False
     raise ValueError(alg)
+
+
+def _compiled(steps: int, compiled) -> bool:
+    """src/algorithms.py:55-58: compiled kernels from 20 000 steps up."""
+    return steps >= 20_000 if compiled is None else bool(compiled)
 
 
 def brute_force(rows):

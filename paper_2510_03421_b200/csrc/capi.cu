@@ -1,5 +1,6 @@
 // extern "C" entry points of libpermanent_b200.so (include/permanent_b200.h).
 #include <algorithm>
+#include <cmath>
 
 #include "engine.cuh"
 
@@ -7,6 +8,10 @@ using namespace permb200;
 
 namespace permb200 {
 const char* last_error();
+int int_permanent(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, int64_t* out,
+                  int* fits_int64, void* stream);
+int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t lda, int dev_ptr,
+                   uint64_t step_budget, double* out, int64_t* ivalue, void* stream);
 }
 
 namespace {
@@ -30,12 +35,27 @@ int check_shape(int alg, int m, int n) {
   return PERM_OK;
 }
 
+// Rectangular Ryser: the all-subsets Gray walk costs 2^n steps, the
+// reference's combination order sum_{s<=m} C(n,s); the latter wins for very
+// rectangular shapes despite its heavier per-step update.
+bool ryser_rect_use_comb(int m, int n) {
+  if (m >= n) return false;
+  long double c = 0, b = 1;  // running C(n, s)
+  for (int s = 1; s <= m; ++s) {
+    b = b * (n - s + 1) / s;
+    c += b;
+  }
+  return c * 8.0L < std::ldexp(1.0L, n);
+}
+
 // Single permanent through the walk engine; returns normalized value.
 int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out,
                 double* magsum, void* stream_) {
   clear_error();
   int st = check_shape(alg, m, n);
   if (st) return st;
+  if (alg == PERM_ALG_RYSER && magsum == nullptr && ryser_rect_use_comb(m, n))
+    return comb_permanent(true, cplx ? 1 : 0, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream_);
   cudaStream_t stream = pick_stream(stream_);
   HostMat A;
   st = load_matrix(m, n, a, lda, dev_ptr, cplx, &A, stream);
@@ -167,6 +187,40 @@ int perm_ryser_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, doub
 int perm_ryser_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
                     void* stream) {
   return walk_single(PERM_ALG_RYSER, true, m, n, a, lda, dev_ptr, out, magsum, stream);
+}
+
+int perm_glynn_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, int64_t* out,
+                   int* fits_int64, void* stream) {
+  return int_permanent(PERM_ALG_GLYNN, m, n, a, lda, dev_ptr, width, out, fits_int64, stream);
+}
+int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, int64_t* out,
+                   int* fits_int64, void* stream) {
+  if (width == 64 && m < n && m >= 1) {
+    // the reference's rectangular int kernel walks combinations
+    // lexicographically (src/_kernels.py:265-365); its overflow flag depends
+    // on that order, so replay it
+    int64_t v = 0;
+    int st = comb_permanent(true, 2, m, n, a, lda, dev_ptr, UINT64_MAX, nullptr, &v, stream);
+    if (st) return st;
+    out[0] = v;
+    out[1] = v < 0 ? -1 : 0;
+    if (fits_int64) *fits_int64 = 1;
+    return PERM_OK;
+  }
+  return int_permanent(PERM_ALG_RYSER, m, n, a, lda, dev_ptr, width, out, fits_int64, stream);
+}
+
+int perm_comb_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t step_budget, double* out,
+                  void* stream) {
+  return comb_permanent(false, 0, m, n, a, lda, dev_ptr, step_budget, out, nullptr, stream);
+}
+int perm_comb_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t step_budget, double* out,
+                   void* stream) {
+  return comb_permanent(false, 1, m, n, a, lda, dev_ptr, step_budget, out, nullptr, stream);
+}
+int perm_comb_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, uint64_t step_budget, int64_t* out,
+                  void* stream) {
+  return comb_permanent(false, 2, m, n, a, lda, dev_ptr, step_budget, nullptr, out, stream);
 }
 
 uint64_t perm_walk_steps(int alg, int m, int n) {

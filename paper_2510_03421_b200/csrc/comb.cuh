@@ -1,0 +1,362 @@
+// Combination- and permutation-ordered kernels:
+//
+//  * ryser_comb_kernel: the binomial-weighted rectangular Ryser of
+//    src/_kernels.py:226-262 (float) / :265-365 (checked int64), walking the
+//    size-s column combinations in the reference's lexicographic order.  Each
+//    thread unranks the first combination of its rank range and advances with
+//    the reference's suffix-incremental row-sum update, so the int64 checks
+//    (including every intermediate row-sum value of each transition) are
+//    exactly the reference's.  Cost sum_{s<=m} C(n,s): far below the 2^n of
+//    the all-subsets Gray walk for very rectangular shapes.
+//
+//  * comb_dfs_kernel: the combinatoric algorithm of src/_kernels.py:28-56 /
+//    :59-108 (depth-first over m-permutations with prefix products, zero
+//    partial products pruned).  The DFS tree is cut at depth D; thread t owns
+//    the t-th depth-D prefix in lexicographic order and runs the reference's
+//    DFS below it.  Float partials are compensated; checked-int partials are
+//    (S, min prefix, max prefix, flag) summaries combined in DFS order.
+#pragma once
+#include "int_walk.cuh"
+
+namespace permb200 {
+
+constexpr int kCombThreads = 128;
+
+enum CombMode { kCombF64 = 0, kCombC128 = 1, kCombI64 = 2 };
+
+struct CombArgs {
+  const void* a;          // m x n row-major (double / cd / int64)
+  const uint64_t* binom;  // [63][63] binomial table C(i, j)
+  int m, n, s;            // ryser: subset size s
+  uint64_t total;         // number of items (combinations / prefixes)
+  uint64_t per_thread;    // items per thread
+  int depth;              // comb_dfs: prefix depth D
+  void* out;              // per block partials
+};
+
+__device__ __forceinline__ uint64_t binom_at(const uint64_t* tab, int i, int j) {
+  return (j < 0 || j > i || i < 0) ? 0ull : tab[i * 63 + j];
+}
+
+// ---------------------------------------------------------------- Ryser
+template <int MODE>
+__global__ void __launch_bounds__(kCombThreads) ryser_comb_kernel(CombArgs A) {
+  const int m = A.m, n = A.n, s = A.s;
+  const uint64_t gtid = (uint64_t)blockIdx.x * kCombThreads + threadIdx.x;
+  const uint64_t r0 = gtid * A.per_thread;
+  uint64_t r1 = r0 + A.per_thread;
+  if (r1 > A.total) r1 = A.total;
+  int comb[64];
+  // accumulators
+  double hi = 0, lo = 0, hi_i = 0, lo_i = 0;
+  Summ sm;
+  sm.S = i128_from(0); sm.mn = i128_from(0); sm.mx = i128_from(0); sm.flag = 0;
+  bool have = false;
+  if (r0 < r1) {
+    // unrank r0 (lexicographic, 0-based)
+    uint64_t r = r0;
+    int x = 0;
+    for (int q = 0; q < s; ++q) {
+      for (;;) {
+        const uint64_t cnt = binom_at(A.binom, n - x - 1, s - q - 1);
+        if (r < cnt) { comb[q] = x++; break; }
+        r -= cnt;
+        ++x;
+      }
+    }
+    if constexpr (MODE == kCombI64) {
+      const int64_t* a = static_cast<const int64_t*>(A.a);
+      int64_t rs[64];
+      for (int i = 0; i < m; ++i) {
+        if (r0 == 0) {  // reference initial sums: sequential checked adds
+          int64_t acc = 0;
+          for (int q = 0; q < s; ++q)
+            if (add_ovf(acc, a[i * n + comb[q]], acc)) sm.flag = 1;
+          rs[i] = acc;
+        } else {        // state reached by the previous transition: must fit
+          i128 acc = i128_from(0);
+          for (int q = 0; q < s; ++q) acc = i128_add(acc, i128_from(a[i * n + comb[q]]));
+          if (!i128_fits_i64(acc)) sm.flag = 1;
+          rs[i] = (int64_t)acc.lo;
+        }
+      }
+      // walk [r0, r1); the transition out of r1-1 into r1 is replayed (and
+      // checked) here, the state it produces is re-checked by the next range
+      for (uint64_t rk = r0; rk < r1 && !sm.flag; ++rk) {
+        int64_t p = 1;
+        for (int i = 0; i < m; ++i) {
+          if (rs[i] == 0) { p = 0; break; }
+          int64_t t;
+          if (mul_ovf(p, rs[i], t)) { sm.flag = 1; break; }
+          p = t;
+        }
+        if (sm.flag) break;
+        sm.S = i128_add(sm.S, i128_from(p));
+        if (!have) { sm.mn = sm.S; sm.mx = sm.S; have = true; }
+        else {
+          if (i128_lt(sm.S, sm.mn)) sm.mn = sm.S;
+          if (i128_lt(sm.mx, sm.S)) sm.mx = sm.S;
+        }
+        int pos = s - 1;
+        while (pos >= 0 && comb[pos] == n - s + pos) --pos;
+        if (pos < 0) break;
+        // reference order (src/_kernels.py:319-340): remove comb[pos..s),
+        // then add the new suffix, row by row inside each column
+        for (int q = pos; q < s; ++q)
+          for (int i = 0; i < m; ++i)
+            if (sub_ovf(rs[i], a[i * n + comb[q]], rs[i])) sm.flag = 1;
+        const int v = comb[pos] + 1;
+        for (int q = pos; q < s; ++q) {
+          comb[q] = v + (q - pos);
+          for (int i = 0; i < m; ++i)
+            if (add_ovf(rs[i], a[i * n + comb[q]], rs[i])) sm.flag = 1;
+        }
+      }
+    } else {
+      using T = typename std::conditional<MODE == kCombF64, double, cd>::type;
+      const T* a = static_cast<const T*>(A.a);
+      T rs[64];
+      for (int i = 0; i < m; ++i) {
+        T acc = Num<T>::zero();
+        for (int q = 0; q < s; ++q) acc = Num<T>::add(acc, a[i * n + comb[q]]);
+        rs[i] = acc;
+      }
+      T chunk = Num<T>::zero();
+      int cnt = 0;
+      for (uint64_t rk = r0; rk < r1; ++rk) {
+        T p = rs[0];
+        for (int i = 1; i < m; ++i) p = Num<T>::mul(p, rs[i]);
+        chunk = Num<T>::add(chunk, p);
+        if (++cnt == 1024) {
+          dd_acc(hi, lo, Num<T>::re(chunk));
+          dd_acc(hi_i, lo_i, Num<T>::im(chunk));
+          chunk = Num<T>::zero();
+          cnt = 0;
+        }
+        if (rk + 1 == r1) break;
+        int pos = s - 1;
+        while (pos >= 0 && comb[pos] == n - s + pos) --pos;
+        for (int q = pos; q < s; ++q)
+          for (int i = 0; i < m; ++i) rs[i] = Num<T>::sub(rs[i], a[i * n + comb[q]]);
+        const int v = comb[pos] + 1;
+        for (int q = pos; q < s; ++q) {
+          comb[q] = v + (q - pos);
+          for (int i = 0; i < m; ++i) rs[i] = Num<T>::add(rs[i], a[i * n + comb[q]]);
+        }
+      }
+      dd_acc(hi, lo, Num<T>::re(chunk));
+      dd_acc(hi_i, lo_i, Num<T>::im(chunk));
+    }
+  }
+  // ---- block reduction (ordered for the checked mode)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (MODE == kCombI64) {
+    if (!have) {
+      sm.mn.lo = ~0ull; sm.mn.hi = 0x3fffffffffffffffull;
+      sm.mx.lo = 0ull;  sm.mx.hi = 0xc000000000000000ull;
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      Summ o;
+      o.S = shfl_down_i128(sm.S, off);
+      o.mn = shfl_down_i128(sm.mn, off);
+      o.mx = shfl_down_i128(sm.mx, off);
+      o.flag = __shfl_down_sync(0xffffffffu, sm.flag, off);
+      if ((lane & (2 * off - 1)) == 0 && lane + off < 32) sm = summ_cat(sm, o);
+    }
+    __shared__ Summ ws[kCombThreads / 32];
+    if (lane == 0) ws[warp] = sm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Summ t = ws[0];
+      for (int w = 1; w < kCombThreads / 32; ++w) t = summ_cat(t, ws[w]);
+      int64_t* o = static_cast<int64_t*>(A.out) + (size_t)blockIdx.x * 8;
+      o[0] = (int64_t)t.S.lo; o[1] = (int64_t)t.S.hi;
+      o[2] = (int64_t)t.mn.lo; o[3] = (int64_t)t.mn.hi;
+      o[4] = (int64_t)t.mx.lo; o[5] = (int64_t)t.mx.hi;
+      o[6] = t.flag; o[7] = 0;
+    }
+  } else {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      dd_add(hi, lo, __shfl_down_sync(0xffffffffu, hi, off), __shfl_down_sync(0xffffffffu, lo, off));
+      dd_add(hi_i, lo_i, __shfl_down_sync(0xffffffffu, hi_i, off), __shfl_down_sync(0xffffffffu, lo_i, off));
+    }
+    __shared__ double red[kCombThreads / 32][4];
+    if (lane == 0) { red[warp][0] = hi; red[warp][1] = lo; red[warp][2] = hi_i; red[warp][3] = lo_i; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double H = red[0][0], L = red[0][1], H2 = red[0][2], L2 = red[0][3];
+      for (int w = 1; w < kCombThreads / 32; ++w) { dd_add(H, L, red[w][0], red[w][1]); dd_add(H2, L2, red[w][2], red[w][3]); }
+      double* o = static_cast<double*>(A.out) + (size_t)blockIdx.x * 8;
+      o[0] = H; o[1] = L; o[2] = H2; o[3] = L2; o[4] = 0; o[5] = 0; o[6] = 0; o[7] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- combinatoric
+// Prefix of depth D with lexicographic index `idx` among the P(n, D)
+// D-permutations: digit q picks the (idx_q)-th unused column.
+template <int MODE>
+__global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
+  const int m = A.m, n = A.n, D = A.depth;
+  const uint64_t gtid = (uint64_t)blockIdx.x * kCombThreads + threadIdx.x;
+  double hi = 0, lo = 0, hi_i = 0, lo_i = 0;
+  Summ sm;
+  sm.S = i128_from(0); sm.mn = i128_from(0); sm.mx = i128_from(0); sm.flag = 0;
+  bool have = false;
+  using T = typename std::conditional<MODE == kCombF64, double,
+                                      typename std::conditional<MODE == kCombC128, cd, int64_t>::type>::type;
+  const T* a = static_cast<const T*>(A.a);
+  const uint64_t p0 = gtid * A.per_thread;
+  uint64_t p1 = p0 + A.per_thread;
+  if (p1 > A.total) p1 = A.total;
+  for (uint64_t pidx = p0; pidx < p1 && !sm.flag; ++pidx) {
+    // decode prefix: mixed radix (n, n-1, ..., n-D+1), most significant first
+    int choice[64];
+    bool used[64];
+    for (int j = 0; j < n; ++j) used[j] = false;
+    {
+      uint64_t rem = pidx;
+      uint64_t radix_prod = 1;
+      for (int q = 1; q < D; ++q) radix_prod *= (uint64_t)(n - q);
+      for (int q = 0; q < D; ++q) {
+        const uint64_t digit = rem / radix_prod;
+        rem -= digit * radix_prod;
+        if (q + 1 < D) radix_prod /= (uint64_t)(n - q - 1);
+        int c = -1;
+        uint64_t k = digit;
+        for (int j = 0; j < n; ++j)
+          if (!used[j]) {
+            if (k == 0) { c = j; break; }
+            --k;
+          }
+        choice[q] = c;
+        used[c] = true;
+      }
+    }
+    // prefix products (checked / pruned exactly like the reference DFS)
+    T prod[65];
+    bool dead = false;
+    if constexpr (MODE == kCombI64) prod[0] = 1; else prod[0] = Num<T>::one();
+    for (int q = 0; q < D; ++q) {
+      T p;
+      if constexpr (MODE == kCombI64) {
+        if (prod[q] != 0 && a[q * n + choice[q]] != 0) {
+          if (mul_ovf(prod[q], a[q * n + choice[q]], p)) { sm.flag = 1; dead = true; break; }
+        } else {
+          p = prod[q] * a[q * n + choice[q]];
+        }
+      } else {
+        p = Num<T>::mul(prod[q], a[q * n + choice[q]]);
+      }
+      if (q == m - 1) {  // leaf inside the prefix (D == m)
+        if constexpr (MODE == kCombI64) {
+          sm.S = i128_add(sm.S, i128_from(p));
+          if (!have) { sm.mn = sm.S; sm.mx = sm.S; have = true; }
+          else { if (i128_lt(sm.S, sm.mn)) sm.mn = sm.S; if (i128_lt(sm.mx, sm.S)) sm.mx = sm.S; }
+        } else {
+          dd_acc(hi, lo, Num<T>::re(p));
+          dd_acc(hi_i, lo_i, Num<T>::im(p));
+        }
+        dead = true;
+        break;
+      }
+      bool zero;
+      if constexpr (MODE == kCombI64) zero = (p == 0);
+      else if constexpr (MODE == kCombF64) zero = (p == 0.0);
+      else zero = (p.x == 0.0 && p.y == 0.0);
+      if (zero) { dead = true; break; }  // src/_kernels.py:52 prune
+      prod[q + 1] = p;
+    }
+    if (dead) continue;
+    // DFS below the prefix (src/_kernels.py:37-55 with d starting at D)
+    int ch[64];
+    for (int q = 0; q < m; ++q) ch[q] = -1;
+    int d = D;
+    T chunk;
+    if constexpr (MODE == kCombI64) chunk = 0; else chunk = Num<T>::zero();
+    while (d >= D) {
+      int j = ch[d];
+      if (j >= 0) used[j] = false;
+      ++j;
+      while (j < n && used[j]) ++j;
+      if (j >= n) { ch[d] = -1; --d; continue; }
+      ch[d] = j;
+      T p;
+      if constexpr (MODE == kCombI64) {
+        if (mul_ovf(prod[d], a[d * n + j], p)) { sm.flag = 1; break; }
+      } else {
+        p = Num<T>::mul(prod[d], a[d * n + j]);
+      }
+      if (d == m - 1) {
+        if constexpr (MODE == kCombI64) {
+          sm.S = i128_add(sm.S, i128_from(p));
+          if (!have) { sm.mn = sm.S; sm.mx = sm.S; have = true; }
+          else { if (i128_lt(sm.S, sm.mn)) sm.mn = sm.S; if (i128_lt(sm.mx, sm.S)) sm.mx = sm.S; }
+        } else {
+          chunk = Num<T>::add(chunk, p);
+        }
+      } else {
+        bool zero;
+        if constexpr (MODE == kCombI64) zero = (p == 0);
+        else if constexpr (MODE == kCombF64) zero = (p == 0.0);
+        else zero = (p.x == 0.0 && p.y == 0.0);
+        if (!zero) {
+          used[j] = true;
+          prod[d + 1] = p;
+          ++d;
+        }
+      }
+    }
+    if constexpr (MODE != kCombI64) {
+      dd_acc(hi, lo, Num<T>::re(chunk));
+      dd_acc(hi_i, lo_i, Num<T>::im(chunk));
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (MODE == kCombI64) {
+    if (!have) {
+      sm.mn.lo = ~0ull; sm.mn.hi = 0x3fffffffffffffffull;
+      sm.mx.lo = 0ull;  sm.mx.hi = 0xc000000000000000ull;
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      Summ o;
+      o.S = shfl_down_i128(sm.S, off);
+      o.mn = shfl_down_i128(sm.mn, off);
+      o.mx = shfl_down_i128(sm.mx, off);
+      o.flag = __shfl_down_sync(0xffffffffu, sm.flag, off);
+      if ((lane & (2 * off - 1)) == 0 && lane + off < 32) sm = summ_cat(sm, o);
+    }
+    __shared__ Summ ws[kCombThreads / 32];
+    if (lane == 0) ws[warp] = sm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Summ t = ws[0];
+      for (int w = 1; w < kCombThreads / 32; ++w) t = summ_cat(t, ws[w]);
+      int64_t* o = static_cast<int64_t*>(A.out) + (size_t)blockIdx.x * 8;
+      o[0] = (int64_t)t.S.lo; o[1] = (int64_t)t.S.hi;
+      o[2] = (int64_t)t.mn.lo; o[3] = (int64_t)t.mn.hi;
+      o[4] = (int64_t)t.mx.lo; o[5] = (int64_t)t.mx.hi;
+      o[6] = t.flag; o[7] = 0;
+    }
+  } else {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      dd_add(hi, lo, __shfl_down_sync(0xffffffffu, hi, off), __shfl_down_sync(0xffffffffu, lo, off));
+      dd_add(hi_i, lo_i, __shfl_down_sync(0xffffffffu, hi_i, off), __shfl_down_sync(0xffffffffu, lo_i, off));
+    }
+    __shared__ double red[kCombThreads / 32][4];
+    if (lane == 0) { red[warp][0] = hi; red[warp][1] = lo; red[warp][2] = hi_i; red[warp][3] = lo_i; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double H = red[0][0], L = red[0][1], H2 = red[0][2], L2 = red[0][3];
+      for (int w = 1; w < kCombThreads / 32; ++w) { dd_add(H, L, red[w][0], red[w][1]); dd_add(H2, L2, red[w][2], red[w][3]); }
+      double* o = static_cast<double*>(A.out) + (size_t)blockIdx.x * 8;
+      o[0] = H; o[1] = L; o[2] = H2; o[3] = L2; o[4] = 0; o[5] = 0; o[6] = 0; o[7] = 0;
+    }
+  }
+}
+
+}  // namespace permb200

@@ -1,0 +1,214 @@
+// Host side of the combination-ordered Ryser and the combinatoric DFS.
+#include <algorithm>
+#include <cmath>
+
+#include "comb.cuh"
+#include "engine.cuh"
+
+namespace permb200 {
+
+typedef __int128 s128;
+
+static uint64_t nperm(int n, int k) {  // P(n, k), saturating
+  unsigned __int128 r = 1;
+  for (int i = 0; i < k; ++i) {
+    r *= (unsigned)(n - i);
+    if (r > (unsigned __int128)UINT64_MAX) return UINT64_MAX;
+  }
+  return (uint64_t)r;
+}
+
+static const std::vector<uint64_t>& binom_table() {
+  static std::vector<uint64_t> t;
+  if (t.empty()) {
+    t.assign(63 * 63, 0);
+    for (int i = 0; i < 63; ++i) {
+      t[i * 63] = 1;
+      for (int j = 1; j <= i; ++j) t[i * 63 + j] = t[(i - 1) * 63 + j - 1] + (j <= i - 1 ? t[(i - 1) * 63 + j] : 0);
+    }
+  }
+  return t;
+}
+
+struct CombRun {
+  void* buf = nullptr;
+  ~CombRun() {
+    if (buf) cudaFree(buf);
+  }
+};
+
+static int target_threads() {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return nsm * 4 * kCombThreads;
+}
+
+// Launch one ryser_comb / comb_dfs kernel and return per-block partials.
+template <int MODE>
+static int launch_comb(bool ryser, const void* dA, const uint64_t* dB, int m, int n, int s, int depth,
+                       uint64_t total, void* dOut, std::vector<int64_t>* host, cudaStream_t stream) {
+  const uint64_t thr = (uint64_t)target_threads();
+  uint64_t per = (total + thr - 1) / thr;
+  if (per < 1) per = 1;
+  const uint64_t nthreads = (total + per - 1) / per;
+  const uint64_t blocks = (nthreads + kCombThreads - 1) / kCombThreads;
+  CombArgs a;
+  a.a = dA;
+  a.binom = dB;
+  a.m = m;
+  a.n = n;
+  a.s = s;
+  a.total = total;
+  a.per_thread = per;
+  a.depth = depth;
+  a.out = dOut;
+  if (ryser) ryser_comb_kernel<MODE><<<(unsigned)blocks, kCombThreads, 0, stream>>>(a);
+  else comb_dfs_kernel<MODE><<<(unsigned)blocks, kCombThreads, 0, stream>>>(a);
+  PERM_CUDA_TRY(cudaGetLastError());
+  host->resize(blocks * 8);
+  PERM_CUDA_TRY(cudaMemcpyAsync(host->data(), dOut, blocks * 64, cudaMemcpyDeviceToHost, stream));
+  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  return PERM_OK;
+}
+
+// Ordered combine of checked summaries; false on overflow.
+static bool combine_checked(const std::vector<int64_t>& h, s128* total) {
+  s128 G = 0;
+  const s128 lo = (s128)INT64_MIN, hi = (s128)INT64_MAX;
+  for (size_t b = 0; b * 8 < h.size(); ++b) {
+    const int64_t* o = &h[b * 8];
+    auto get = [&](int q) { return (s128)(((unsigned __int128)(uint64_t)o[q + 1] << 64) | (uint64_t)o[q]); };
+    if (o[6]) return false;
+    if (G + get(2) < lo || G + get(4) > hi) return false;
+    G += get(0);
+  }
+  *total = G;
+  return true;
+}
+
+static void combine_float(const std::vector<int64_t>& h, double* re_h, double* re_l, double* im_h, double* im_l) {
+  for (size_t b = 0; b * 8 < h.size(); ++b) {
+    const double* o = reinterpret_cast<const double*>(&h[b * 8]);
+    dd_add(*re_h, *re_l, o[0], o[1]);
+    dd_add(*im_h, *im_l, o[2], o[3]);
+  }
+}
+
+// mode 0 f64, 1 c128, 2 int64 checked.  Float: out[0..1] = re, im.
+// Int: *ivalue, PERM_OVERFLOW on reference overflow.
+int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t lda, int dev_ptr,
+                   uint64_t step_budget, double* out, int64_t* ivalue, void* stream_) {
+  clear_error();
+  if (m < 1 || n < 1) {
+    set_error("matrix must have m >= 1 and n >= 1");
+    return PERM_BAD_SHAPE;
+  }
+  if (m > n || n > 62) {
+    set_error(m > n ? "need m <= n; transpose first" : "more than 62 columns");
+    return PERM_BAD_SHAPE;
+  }
+  if (!ryser) {  // src/algorithms.py:78-84
+    const uint64_t perms = nperm(n, m);
+    if (perms > step_budget) {
+      set_error("combinatoric step budget exceeded");
+      return PERM_BUDGET;
+    }
+  }
+  cudaStream_t stream = pick_stream(stream_);
+  const int esz = (mode == 1) ? 16 : 8;
+  std::vector<unsigned char> hA((size_t)m * n * esz);
+  if (dev_ptr) {
+    PERM_CUDA_TRY(cudaMemcpy2DAsync(hA.data(), (size_t)n * esz, a, (size_t)lda * esz, (size_t)n * esz, m,
+                                    cudaMemcpyDeviceToHost, stream));
+    PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  } else {
+    for (int i = 0; i < m; ++i)
+      std::memcpy(&hA[(size_t)i * n * esz], static_cast<const unsigned char*>(a) + (size_t)i * lda * esz,
+                  (size_t)n * esz);
+  }
+  const auto& bt = binom_table();
+  // device buffers: matrix, binomials, partials
+  const uint64_t thr = (uint64_t)target_threads();
+  const size_t max_blocks = (thr + kCombThreads - 1) / kCombThreads + 1;
+  const size_t bytes = hA.size() + bt.size() * 8 + max_blocks * 64 + 256;
+  CombRun run;
+  PERM_CUDA_TRY(cudaMallocAsync(&run.buf, bytes, stream));
+  unsigned char* base = static_cast<unsigned char*>(run.buf);
+  void* dA = base;
+  uint64_t* dB = reinterpret_cast<uint64_t*>(base + ((hA.size() + 15) & ~(size_t)15));
+  void* dOut = dB + bt.size();
+  PERM_CUDA_TRY(cudaMemcpyAsync(dA, hA.data(), hA.size(), cudaMemcpyHostToDevice, stream));
+  PERM_CUDA_TRY(cudaMemcpyAsync(dB, bt.data(), bt.size() * 8, cudaMemcpyHostToDevice, stream));
+  std::vector<int64_t> h;
+  int st = PERM_OK;
+  if (ryser) {
+    // src/_kernels.py:226-262 / 265-365: s = m..1, total += w[s] * size_sum
+    double th = 0, tl = 0, ih = 0, il = 0;
+    int64_t itotal = 0;
+    bool ovf = false;
+    for (int s = m; s >= 1 && !ovf; --s) {
+      const uint64_t total = bt[n * 63 + s];
+      int64_t c = (int64_t)bt[(n - s) * 63 + (m - s)];
+      const int64_t w = ((m - s) & 1) ? -c : c;
+      if (mode == 2) {
+        st = launch_comb<kCombI64>(true, dA, dB, m, n, s, 0, total, dOut, &h, stream);
+        if (st) return st;
+        s128 size_sum;
+        if (!combine_checked(h, &size_sum)) { ovf = true; break; }
+        int64_t ss = (int64_t)size_sum, p;
+        if (__builtin_mul_overflow(w, ss, &p) || __builtin_add_overflow(itotal, p, &itotal)) ovf = true;
+      } else {
+        double rh = 0, rl = 0, jh = 0, jl = 0;
+        st = (mode == 0) ? launch_comb<kCombF64>(true, dA, dB, m, n, s, 0, total, dOut, &h, stream)
+                         : launch_comb<kCombC128>(true, dA, dB, m, n, s, 0, total, dOut, &h, stream);
+        if (st) return st;
+        combine_float(h, &rh, &rl, &jh, &jl);
+        const double wd = (double)w;
+        // w * size_sum in double-double (w exact up to 2^53)
+        dd_add(th, tl, wd * rh, std::fma(wd, rh, -(wd * rh)) + wd * rl);
+        dd_add(ih, il, wd * jh, std::fma(wd, jh, -(wd * jh)) + wd * jl);
+      }
+    }
+    if (mode == 2) {
+      if (ovf) {
+        set_error("an int64 intermediate overflowed (reference semantics)");
+        return PERM_OVERFLOW;
+      }
+      *ivalue = itotal;
+    } else {
+      out[0] = th + tl;
+      if (mode == 1) out[1] = ih + il;
+    }
+  } else {
+    // prefix depth: enough prefixes to fill the device, at most m
+    int D = 0;
+    while (D < m && nperm(n, D) < thr * 4) ++D;
+    if (D < 1) D = 1;
+    const uint64_t total = nperm(n, D);
+    if (mode == 2) {
+      st = launch_comb<kCombI64>(false, dA, dB, m, n, 0, D, total, dOut, &h, stream);
+      if (st) return st;
+      s128 t;
+      if (!combine_checked(h, &t)) {
+        set_error("an int64 intermediate overflowed (reference semantics)");
+        return PERM_OVERFLOW;
+      }
+      *ivalue = (int64_t)t;
+    } else {
+      st = (mode == 0) ? launch_comb<kCombF64>(false, dA, dB, m, n, 0, D, total, dOut, &h, stream)
+                       : launch_comb<kCombC128>(false, dA, dB, m, n, 0, D, total, dOut, &h, stream);
+      if (st) return st;
+      double rh = 0, rl = 0, jh = 0, jl = 0;
+      combine_float(h, &rh, &rl, &jh, &jl);
+      out[0] = rh + rl;
+      if (mode == 1) out[1] = jh + jl;
+    }
+  }
+  PERM_CUDA_TRY(cudaFreeAsync(run.buf, stream));
+  run.buf = nullptr;
+  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  return PERM_OK;
+}
+
+}  // namespace permb200

@@ -1,0 +1,317 @@
+// Exact integer Gray walks (north_star item 3), two modes:
+//
+// CHECKED (reference semantics).  Replays the reference's pre-checked int64
+// arithmetic (src/_kernels.py:148-218 ryser_sq_int, :412-523 glynn_sq_int,
+// :580-697 glynn_rect_int).  The reference returns (0, True) at the first
+// int64 overflow; since every value before that point is exact, its flag is
+// the OR, over the exact computation, of "this checked operation left int64".
+// That OR is evaluated in parallel: each thread replays one contiguous Gray
+// range with checked state updates and checked prefix products (stopping at
+// the first zero factor exactly as the reference does), and summarizes its
+// terms as (S, min prefix, max prefix) in 128-bit.  Ranges combine with the
+// associative (S1,m1,M1)+(S2,m2,M2) = (S1+S2, min(m1,S1+m2), max(M1,S1+M2)),
+// in Gray order (lanes, then warps, then blocks on the host), so the running
+// total's int64 excursions are detected exactly as the sequential walk would.
+//
+// WRAP (exact int128, opt-in).  Mod-2^128 ring arithmetic: the
+// walk sum is exact whenever the true value lies in (-2^127, 2^127), which the
+// host certifies with an FP64 run plus its magnitude-sum error bound.
+#pragma once
+#include "common.cuh"
+
+namespace permb200 {
+
+constexpr int kIntThreads = 128;
+constexpr int kIntWarps = kIntThreads / 32;
+
+struct IntWalkArgs {
+  const int64_t* v0;   // [P]
+  const int64_t* U;    // [B][P]
+  const int64_t* w;    // [wlen] (weighted wrap walks)
+  int P, B, log2L, wlen;
+  uint64_t k_begin;
+  uint64_t nchunks;
+  int64_t* out;        // per block: 8 int64 slots
+};
+
+// --- CHECKED summary combine ---------------------------------------------
+struct Summ {
+  i128 S, mn, mx;
+  int flag;
+};
+__device__ __forceinline__ Summ summ_cat(const Summ& a, const Summ& b) {  // a precedes b
+  Summ r;
+  r.flag = a.flag | b.flag;
+  r.S = i128_add(a.S, b.S);
+  i128 bm = i128_add(a.S, b.mn), bM = i128_add(a.S, b.mx);
+  r.mn = i128_lt(bm, a.mn) ? bm : a.mn;
+  r.mx = i128_lt(a.mx, bM) ? bM : a.mx;
+  return r;
+}
+__device__ __forceinline__ i128 shfl_down_i128(i128 x, int off) {
+  i128 r;
+  r.lo = __shfl_down_sync(0xffffffffu, x.lo, off);
+  r.hi = __shfl_down_sync(0xffffffffu, x.hi, off);
+  return r;
+}
+
+__device__ __forceinline__ bool add_ovf(int64_t a, int64_t b, int64_t& r) {
+  r = (int64_t)((uint64_t)a + (uint64_t)b);
+  return ((a ^ r) & (b ^ r)) < 0;
+}
+__device__ __forceinline__ bool sub_ovf(int64_t a, int64_t b, int64_t& r) {
+  r = (int64_t)((uint64_t)a - (uint64_t)b);
+  return ((a ^ b) & (a ^ r)) < 0;
+}
+__device__ __forceinline__ bool mul_ovf(int64_t a, int64_t b, int64_t& r) {
+  r = (int64_t)((uint64_t)a * (uint64_t)b);
+  const int64_t hi = __mul64hi(a, b);
+  return hi != (r >> 63);
+}
+
+// One contiguous range of 2^log2L indices per thread; grid covers nchunks exactly.
+static __global__ void __launch_bounds__(kIntThreads) int_walk_checked_kernel(IntWalkArgs a) {
+  const uint64_t gtid = (uint64_t)blockIdx.x * kIntThreads + threadIdx.x;
+  const int P = a.P, B = a.B;
+  Summ s;
+  s.S = i128_from(0);
+  s.mn = i128_from(0);
+  s.mx = i128_from(0);
+  s.flag = 0;
+  bool have = false;
+  if (gtid < a.nchunks) {
+    const uint64_t k0 = a.k_begin + (gtid << a.log2L);
+    const uint64_t k1 = k0 + (1ull << a.log2L);
+    int64_t v[64];
+    const uint64_t g0 = k0 ^ (k0 >> 1);
+    for (int j = 0; j < P; ++j) {
+      i128 acc = i128_from(a.v0[j]);
+      for (int t = 0; t < B; ++t)
+        if ((g0 >> t) & 1) acc = i128_add(acc, i128_from(a.U[(size_t)t * P + j]));
+      if (!i128_fits_i64(acc)) s.flag = 1;  // the reference's update producing this state overflowed
+      v[j] = (int64_t)acc.lo;
+    }
+    for (uint64_t k = k0; k < k1 && !s.flag; ++k) {
+      if (k != k0) {
+        const int t = __ffsll((long long)k) - 1;
+        const bool set = ((k ^ (k >> 1)) >> t) & 1;
+        const int64_t* u = a.U + (size_t)t * P;
+        for (int j = 0; j < P; ++j) {
+          int64_t r;
+          bool o = set ? add_ovf(v[j], u[j], r) : sub_ovf(v[j], u[j], r);
+          if (o) s.flag = 1;
+          v[j] = r;
+        }
+        if (s.flag) break;
+      }
+      int64_t p = 1;
+      for (int j = 0; j < P; ++j) {  // src/_kernels.py:486-507: stop at the first zero factor
+        if (v[j] == 0) { p = 0; break; }
+        int64_t r;
+        if (mul_ovf(p, v[j], r)) { s.flag = 1; break; }
+        p = r;
+      }
+      if (s.flag) break;
+      i128 x = i128_from(p);
+      if (k & 1) x = i128_sub(i128_from(0), x);
+      s.S = i128_add(s.S, x);
+      if (!have) {
+        s.mn = s.S;
+        s.mx = s.S;
+        have = true;
+      } else {
+        if (i128_lt(s.S, s.mn)) s.mn = s.S;
+        if (i128_lt(s.mx, s.S)) s.mx = s.S;
+      }
+    }
+  }
+  // empty summaries (threads past nchunks) are identities: S = 0, mn = mx = 0
+  // would wrongly clamp; give them mn = +big, mx = -big instead.
+  if (!have) {
+    s.mn.lo = ~0ull; s.mn.hi = 0x3fffffffffffffffull;       // +2^126-ish
+    s.mx.lo = 0ull;  s.mx.hi = 0xc000000000000000ull;       // -2^126
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Summ o;
+    o.S = shfl_down_i128(s.S, off);
+    o.mn = shfl_down_i128(s.mn, off);
+    o.mx = shfl_down_i128(s.mx, off);
+    o.flag = __shfl_down_sync(0xffffffffu, s.flag, off);
+    // lane i combines with lane i+off only when aligned (ordered tree)
+    if ((lane & (2 * off - 1)) == 0 && lane + off < 32) s = summ_cat(s, o);
+  }
+  __shared__ Summ ws[kIntWarps];
+  if (lane == 0) ws[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Summ t = ws[0];
+    for (int w = 1; w < kIntWarps; ++w) t = summ_cat(t, ws[w]);
+    int64_t* o = a.out + (size_t)blockIdx.x * 8;
+    o[0] = (int64_t)t.S.lo; o[1] = (int64_t)t.S.hi;
+    o[2] = (int64_t)t.mn.lo; o[3] = (int64_t)t.mn.hi;
+    o[4] = (int64_t)t.mx.lo; o[5] = (int64_t)t.mx.hi;
+    o[6] = t.flag; o[7] = 0;
+  }
+}
+
+// ---- WRAP: exact mod-2^128 walk -------------------------------------------
+// Generic (runtime P, optional popcount weights); grid-stride over chunks.
+static __global__ void __launch_bounds__(kIntThreads) int_walk_wrap_generic_kernel(IntWalkArgs a, int weighted) {
+  const int P = a.P, B = a.B;
+  i128 acc = i128_from(0);
+  const uint64_t nthr = (uint64_t)gridDim.x * kIntThreads;
+  for (uint64_t c = (uint64_t)blockIdx.x * kIntThreads + threadIdx.x; c < a.nchunks; c += nthr) {
+    const uint64_t k0 = a.k_begin + (c << a.log2L);
+    const uint64_t k1 = k0 + (1ull << a.log2L);
+    int64_t v[64];
+    const uint64_t g0 = k0 ^ (k0 >> 1);
+    for (int j = 0; j < P; ++j) {
+      int64_t x = a.v0[j];
+      for (int t = 0; t < B; ++t)
+        if ((g0 >> t) & 1) x += a.U[(size_t)t * P + j];
+      v[j] = x;
+    }
+    int pc = __popcll(g0);
+    for (uint64_t k = k0; k < k1; ++k) {
+      if (k != k0) {
+        const int t = __ffsll((long long)k) - 1;
+        const bool set = ((k ^ (k >> 1)) >> t) & 1;
+        const int64_t* u = a.U + (size_t)t * P;
+        if (set) for (int j = 0; j < P; ++j) v[j] += u[j];
+        else for (int j = 0; j < P; ++j) v[j] -= u[j];
+        pc += set ? 1 : -1;
+      }
+      i128 p = i128_from(v[0]);
+      for (int j = 1; j < P; ++j) p = i128_mul_s64(p, v[j]);
+      if (weighted) acc = i128_add(acc, i128_mul_s64(p, a.w[pc]));
+      else acc = (k & 1) ? i128_sub(acc, p) : i128_add(acc, p);
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) acc = i128_add(acc, shfl_down_i128(acc, off));
+  __shared__ i128 ws[kIntWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) ws[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i128 t = ws[0];
+    for (int w = 1; w < kIntWarps; ++w) t = i128_add(t, ws[w]);
+    a.out[(size_t)blockIdx.x * 2] = (int64_t)t.lo;
+    a.out[(size_t)blockIdx.x * 2 + 1] = (int64_t)t.hi;
+  }
+}
+
+// Fast unweighted WRAP walk, compile-time P; factors multiplied exactly in
+// int64 in groups of 8 (host guarantees |state|^8 < 2^63), groups folded
+// into the 128-bit product.  Same 8-step unrolled schedule as walk_kernel.
+template <int P>
+__device__ __forceinline__ i128 int_prod_g8(const int64_t (&v)[P]) {
+  constexpr int NG = (P + 7) / 8;
+  int64_t g[NG];
+#pragma unroll
+  for (int q = 0; q < NG; ++q) {
+    int64_t x = v[8 * q];
+#pragma unroll
+    for (int j = 8 * q + 1; j < 8 * q + 8 && j < P; ++j) x *= v[j];
+    g[q] = x;
+  }
+  i128 p = i128_from(g[0]);
+#pragma unroll
+  for (int q = 1; q < NG; ++q) p = i128_mul_s64(p, g[q]);
+  return p;
+}
+
+template <int P>
+__device__ __forceinline__ void irow(int64_t (&v)[P], const int64_t* __restrict__ row, int64_t sign) {
+  // v += sign * row, sign in {+1, -1}: two's-complement negate via xor/sub
+  const int64_t msk = sign >> 63;  // 0 or -1
+#pragma unroll
+  for (int j = 0; j < P; ++j) v[j] += (((const volatile int64_t*)row)[j] ^ msk) - msk;
+}
+template <int P>
+__device__ __forceinline__ void irow_add(int64_t (&v)[P], const int64_t* __restrict__ row) {
+#pragma unroll
+  for (int j = 0; j < P; ++j) v[j] += ((const volatile int64_t*)row)[j];
+}
+template <int P>
+__device__ __forceinline__ void irow_sub(int64_t (&v)[P], const int64_t* __restrict__ row) {
+#pragma unroll
+  for (int j = 0; j < P; ++j) v[j] -= ((const volatile int64_t*)row)[j];
+}
+
+template <int P>
+__global__ void __launch_bounds__(kIntThreads) int_walk_wrap_kernel(IntWalkArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int64_t* sU = reinterpret_cast<int64_t*>(smem_raw);
+  const int B = a.B;
+  for (int i = threadIdx.x; i < B * P; i += kIntThreads) sU[i] = a.U[i];
+  __syncthreads();
+  const uint64_t L = 1ull << a.log2L;
+  const uint64_t nq = L >> 3;
+  i128 acc = i128_from(0);
+  const uint64_t nthr = (uint64_t)gridDim.x * kIntThreads;
+  for (uint64_t c = (uint64_t)blockIdx.x * kIntThreads + threadIdx.x; c < a.nchunks; c += nthr) {
+    const uint64_t k0 = a.k_begin + (c << a.log2L);
+    int64_t v[P];
+    const uint64_t g0 = k0 ^ (k0 >> 1);
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = a.v0[j];
+    for (int t = 0; t < B; ++t)
+      if ((g0 >> t) & 1) irow_add<P>(v, sU + t * P);
+    for (uint64_t q = 0; q < nq; ++q) {
+      const uint64_t l0 = q << 3;
+      if (q) {
+        const int t = __ffsll((long long)l0) - 1;
+        const uint64_t k = k0 + l0;
+        const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
+        irow<P>(v, sU + t * P, set ? 1 : -1);
+      }
+      acc = i128_add(acc, int_prod_g8<P>(v));
+      irow_add<P>(v, sU);
+      acc = i128_sub(acc, int_prod_g8<P>(v));
+      irow_add<P>(v, sU + P);
+      acc = i128_add(acc, int_prod_g8<P>(v));
+      irow_sub<P>(v, sU);
+      acc = i128_sub(acc, int_prod_g8<P>(v));
+      {
+        const int b3 = (int)(((k0 + l0) >> 3) & 1);
+        irow<P>(v, sU + 2 * P, b3 ? -1 : 1);
+      }
+      acc = i128_add(acc, int_prod_g8<P>(v));
+      irow_add<P>(v, sU);
+      acc = i128_sub(acc, int_prod_g8<P>(v));
+      irow_sub<P>(v, sU + P);
+      acc = i128_add(acc, int_prod_g8<P>(v));
+      irow_sub<P>(v, sU);
+      acc = i128_sub(acc, int_prod_g8<P>(v));
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) acc = i128_add(acc, shfl_down_i128(acc, off));
+  __shared__ i128 ws[kIntWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) ws[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i128 t = ws[0];
+    for (int w = 1; w < kIntWarps; ++w) t = i128_add(t, ws[w]);
+    a.out[(size_t)blockIdx.x * 2] = (int64_t)t.lo;
+    a.out[(size_t)blockIdx.x * 2 + 1] = (int64_t)t.hi;
+  }
+}
+
+using walk_fn_i = cudaError_t (*)(const IntWalkArgs&, int blocks, cudaStream_t);
+
+template <int P>
+cudaError_t launch_int_wrap(const IntWalkArgs& a, int blocks, cudaStream_t stream) {
+  const size_t smem = (size_t)a.B * P * sizeof(int64_t);
+  auto kern = int_walk_wrap_kernel<P>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<blocks, kIntThreads, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace permb200

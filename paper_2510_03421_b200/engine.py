@@ -1,0 +1,108 @@
+"""Typed calls into the C ABI (include/permanent_b200.h).
+
+This module is the replacement of the reference's kernel registry
+``_kernels.get_kernel`` (/root/reference/pkg/src/permanent/_kernels.py:718-728):
+the reference returns a raw enumeration kernel and normalizes in
+``algorithms.py``; here each call returns the normalized permanent computed
+on the GPU.  Arrays are host numpy arrays (staged by the engine) or torch
+CUDA tensors (read in place).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+ALG_CODE = {"combinatoric": _lib.ALG_COMBINATORIC, "ryser": _lib.ALG_RYSER, "glynn": _lib.ALG_GLYNN}
+
+
+def _stage(a):
+    """(pointer, lda, dev_ptr, keepalive, stream) for a 2-D array or tensor."""
+    try:
+        import torch
+
+        if isinstance(a, torch.Tensor) and a.is_cuda:
+            t = a.contiguous()
+            if t.dtype == torch.complex128:
+                lda = t.shape[1]
+            else:
+                lda = t.shape[1]
+            return C.c_void_p(t.data_ptr()), lda, 1, t, C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+    except ImportError:  # pragma: no cover
+        pass
+    arr = np.ascontiguousarray(a)
+    return C.c_void_p(arr.ctypes.data), arr.shape[1], 0, arr, None
+
+
+def walk(alg: str, a, magsum: bool = False):
+    """Glynn / Ryser permanent of a float64 or complex128 m x n (m <= n)
+    matrix; returns (value, M) with M the magnitude sum (or None)."""
+    lib = _lib.load()
+    cplx = np.iscomplexobj(a) if not hasattr(a, "is_complex") else a.is_complex()
+    m, n = a.shape
+    ptr, lda, dev, keep, stream = _stage(a)
+    out = _lib.out_buf(2)
+    mg = C.c_double(0.0)
+    fn = getattr(lib, f"perm_{alg}_{'c128' if cplx else 'f64'}")
+    st = fn(m, n, ptr, lda, dev, out, C.byref(mg) if magsum else None, stream)
+    _lib.check(st, f"{alg} {m}x{n}")
+    val = complex(out[0], out[1]) if cplx else float(out[0])
+    return val, (mg.value if magsum else None)
+
+
+def comb(a, step_budget: int):
+    """Combinatoric permanent (float64 / complex128 / checked int64).
+    Returns (value, overflowed); raises ValueError / RuntimeError codes as the
+    C ABI reports them (BUDGET is mapped by the caller)."""
+    lib = _lib.load()
+    m, n = a.shape
+    kind = a.dtype.kind if isinstance(a, np.ndarray) else None
+    ptr, lda, dev, keep, stream = _stage(a)
+    budget = C.c_uint64(min(int(step_budget), (1 << 64) - 1) if step_budget >= 0 else 0)
+    if kind in ("i",):
+        out = (C.c_int64 * 2)()
+        st = lib.perm_comb_i64(m, n, ptr, lda, dev, budget, out, stream)
+        if st == _lib.OVERFLOW:
+            return 0, True, st
+        if st == _lib.BUDGET:
+            return None, False, st
+        _lib.check(st, f"combinatoric {m}x{n}")
+        return int(out[0]), False, st
+    cplx = np.iscomplexobj(a)
+    out = _lib.out_buf(2)
+    fn = lib.perm_comb_c128 if cplx else lib.perm_comb_f64
+    st = fn(m, n, ptr, lda, dev, budget, out, stream)
+    if st == _lib.BUDGET:
+        return None, False, st
+    _lib.check(st, f"combinatoric {m}x{n}")
+    return (complex(out[0], out[1]) if cplx else float(out[0])), False, st
+
+
+def exact_int(alg: str, a: np.ndarray, width: int = 64):
+    """Integer permanent.  width=64: (value, overflowed) with the reference's
+    checked-int64 semantics; width=128: (exact int, not fits_int64), raising
+    OverflowError when the int128 fit certificate fails."""
+    lib = _lib.load()
+    m, n = a.shape
+    ptr, lda, dev, keep, stream = _stage(a)
+    out = (C.c_int64 * 2)()
+    fits = C.c_int(0)
+    fn = lib.perm_glynn_i64 if alg == "glynn" else lib.perm_ryser_i64
+    st = fn(m, n, ptr, lda, dev, width, out, C.byref(fits), stream)
+    if st == _lib.OVERFLOW:
+        if width == 64:
+            return 0, True
+        raise OverflowError(f"exact int128 {alg} {m}x{n}: {_lib.last_error()}")
+    _lib.check(st, f"{alg} int{width} {m}x{n}")
+    v = (int(out[1]) << 64) | (int(out[0]) & ((1 << 64) - 1))
+    return v, (not fits.value)
+
+
+def walk_steps(alg: str, m: int, n: int) -> int:
+    return int(_lib.load().perm_walk_steps(ALG_CODE[alg], m, n))
+
+
+def sm_count() -> int:
+    return int(_lib.load().perm_device_sm_count())

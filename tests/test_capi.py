@@ -1,0 +1,101 @@
+"""The C ABI library: it loads, exports exactly what include/permanent_b200.h
+declares, and its pure-host entry points (sharding plan, partial combine,
+dispatch) behave.  No compute call is made on CPU except to check that the
+product path fails loudly without a GPU (there is no CPU fallback)."""
+from __future__ import annotations
+
+import ctypes as C
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2510_03421_b200 import _lib
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "permanent_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(perm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_abi():
+    syms = declared_symbols()
+    for must in ("perm_glynn_f64", "perm_glynn_c128", "perm_ryser_f64", "perm_ryser_c128",
+                 "perm_comb_f64", "perm_comb_c128", "perm_comb_i64", "perm_glynn_i64",
+                 "perm_ryser_i64", "perm_walk_partial_f64", "perm_walk_finish_f64", "perm_select",
+                 "perm_batch_f64", "perm_batch_c128"):
+        assert must in syms, must
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (perm_[a-z0-9_]+)", out))
+    for s in declared_symbols():
+        assert s in exported, s
+        assert hasattr(lib, s)
+    # and the Python binding table covers the header
+    assert set(declared_symbols()) <= set(_lib.SIGNATURES)
+
+
+def test_version_and_select():
+    lib = _lib.load()
+    assert lib.perm_version() >= 100
+    p = (C.c_double * 8)(-1.0, -0.105, 1.655, 5.0, 1.0, -0.007, -0.199, 13.0)
+    assert lib.perm_select(3, 3, p, 0, 0) == _lib.ALG_COMBINATORIC
+    assert lib.perm_select(20, 20, p, 0, 0) == _lib.ALG_GLYNN
+    assert lib.perm_select(4, 20, p, 0, 0) == _lib.ALG_RYSER
+
+
+@pytest.mark.parametrize("alg,m,n", [(2, 36, 36), (2, 20, 28), (1, 30, 30), (1, 5, 33), (2, 3, 3)])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 7, 8])
+def test_shards_partition_the_walk(alg, m, n, world):
+    lib = _lib.load()
+    steps = lib.perm_walk_steps(alg, m, n)
+    assert steps == (1 << (n - 1) if alg == 2 else 1 << n)
+    prev = 0
+    for r in range(world):
+        b, e = C.c_uint64(), C.c_uint64()
+        assert lib.perm_walk_shard(alg, m, n, r, world, C.byref(b), C.byref(e)) == _lib.OK
+        assert b.value == prev and e.value >= b.value
+        prev = e.value
+    assert prev == steps
+
+
+def test_finish_combines_partials_in_order():
+    """Double-double combine + Glynn normalization of raw partials."""
+    lib = _lib.load()
+    a = np.eye(4)
+    parts = np.zeros((3, 8))
+    parts[:, 0] = [1.0, 2.0**-60, 7.0]  # hi parts
+    out = (C.c_double * 2)()
+    mg = C.c_double()
+    st = lib.perm_walk_finish_f64(2, 4, 4, C.c_void_p(a.ctypes.data), 4, C.c_void_p(parts.ctypes.data), 3,
+                                  out, C.byref(mg))
+    assert st == _lib.OK
+    assert out[0] == (8.0 + 2.0**-60) / 8.0
+
+
+def test_bad_shapes_rejected_by_the_abi():
+    lib = _lib.load()
+    b, e = C.c_uint64(), C.c_uint64()
+    assert lib.perm_walk_shard(2, 5, 3, 0, 1, C.byref(b), C.byref(e)) == _lib.BAD_SHAPE
+    assert lib.perm_walk_shard(2, 3, 63, 0, 1, C.byref(b), C.byref(e)) == _lib.BAD_SHAPE
+    assert lib.perm_walk_shard(2, 3, 3, 2, 2, C.byref(b), C.byref(e)) == _lib.BAD_ARG
+
+
+def test_no_cpu_fallback_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2510_03421_b200 as P
+
+    with pytest.raises(_lib.EngineUnavailable):
+        P.glynn(np.random.default_rng(0).uniform(-1, 1, (5, 5)))

@@ -1,0 +1,266 @@
+"""Parity of the CUDA engine against the reference (golden fixtures made by
+running it, oracle/gen_golden.py) and the CPU oracle.  Needs a B200.
+
+Tolerances (north_star): integer results bit-exact, overflow flags exactly
+the reference's; float64 / complex128 within 1e-10 of the reference under
+the scale-aware metric |x - ref| / max(|x|, |ref|, M), M = the Glynn
+magnitude sum reported by the engine; plain relative
+error (metric (i)) where the reference's own algorithms agree to 1e-10."""
+from __future__ import annotations
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+import paper_2510_03421_b200 as P
+from conftest import GOLDEN, decode_matrix, decode_value, parity_case, rel_err, scaled_err
+from oracle import oracle as O
+from paper_2510_03421_b200 import workloads as W
+from paper_2510_03421_b200.algorithms import AlgorithmId, run_algorithm
+from paper_2510_03421_b200.core import as_matrix
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+FNS = {"combinatoric": P.combinatoric, "ryser": P.ryser, "glynn": P.glynn, "opt": P.opt}
+
+
+def magsum(a):
+    a = np.asarray(a)
+    if a.dtype.kind in "iub":
+        a = a.astype(np.float64)
+    if a.shape[0] > a.shape[1]:
+        a = a.T
+    return P.permanent_with_magsum(as_matrix(a), AlgorithmId.GLYNN)[1]
+
+
+# ------------------------------------------------------------ golden vectors
+def test_parity_json(parity_cases):
+    """The reference's 300 golden vectors through the public API."""
+    for c in parity_cases:
+        a, alg, exp = parity_case(c)
+        got = FNS[alg](a)
+        if isinstance(exp, int):
+            assert type(got) is int and got == exp, (alg, a)
+        else:
+            assert type(got) is type(exp)
+            assert scaled_err(got, exp, magsum(a)) <= TOL, (alg, a.shape, got, exp)
+
+
+def test_reference_cases(ref_cases):
+    """All algorithms x kinds, m <= n <= 9, and the int-overflow KATs:
+    integer values and overflow flags must equal the reference's."""
+    for case in ref_cases:
+        a = decode_matrix(case["matrix"])
+        mat = as_matrix(a)
+        M = None
+        for alg, r in case["results"].items():
+            res = run_algorithm(mat, AlgorithmId(alg))
+            exp = decode_value(r["value"])
+            if a.dtype.kind == "i":
+                assert res.overflowed == r["overflowed"], (alg, a)
+                if not r["overflowed"]:
+                    assert res.value == exp, (alg, a)
+            else:
+                M = magsum(a) if M is None else M
+                assert scaled_err(res.value, exp, M) <= TOL, (alg, a.shape, res.value, exp)
+
+
+def test_int_walk_near_overflow(ref_int_walk):
+    """n = 10..20 0/1 and {-2..2} matrices around the int64 overflow onset:
+    flags and values exactly the reference's; exact int128 always."""
+    for case in ref_int_walk:
+        a = decode_matrix(case["matrix"])
+        exact = int(case["exact"])
+        for alg, r in case["results"].items():
+            res = run_algorithm(as_matrix(a), AlgorithmId(alg))
+            assert res.overflowed == r["overflowed"], (alg, a.shape)
+            if not res.overflowed:
+                assert res.value == exact
+            ex = run_algorithm(as_matrix(a), AlgorithmId(alg), exact="int128")
+            assert ex.value == exact
+
+
+# ----------------------------------------------------- reference KATs (§4)
+def test_known_values():
+    for fn in FNS.values():
+        assert fn([[1, 2, 3], [4, 5, 6], [7, 8, 9]]) == 450
+        assert fn([[1, 2], [3, 4]]) == 10
+        for n in (3, 4):
+            assert fn(np.eye(n, dtype=np.int64)) == 1
+    assert P.combinatoric([[2, 3, 4]]) == 9
+    assert P.ryser([[2, 3, 4]]) == 9
+    assert P.glynn([[5.0, -1.5]]) == pytest.approx(3.5)
+    assert P.ryser(np.ones((2, 4), dtype=np.int64)) == 12
+    assert P.glynn(np.ones((2, 4), dtype=np.int64)) == 12
+    for fn in (P.ryser, P.glynn, P.combinatoric):
+        assert fn([[0, 1, 0], [1, 0, 0]]) == 1
+
+
+def test_integer_overflow_semantics():
+    big = np.array([[2**62, 3], [5, 2**62]], dtype=np.int64)
+    for fn in FNS.values():
+        with pytest.raises(OverflowError):
+            fn(big)
+    a = as_matrix(np.array([[2**30, 1], [1, 2**30]], dtype=np.int64))
+    for alg in AlgorithmId:
+        res = run_algorithm(a, alg)
+        assert not res.overflowed and res.value == 2**60 + 1
+    b = as_matrix(np.array([[2**31, 1], [1, 2**31]], dtype=np.int64))
+    assert run_algorithm(b, AlgorithmId.COMBINATORIC).value == 2**62 + 1
+    assert run_algorithm(b, AlgorithmId.RYSER).value == 2**62 + 1
+    assert run_algorithm(b, AlgorithmId.GLYNN).overflowed
+    # the opt-in exact path returns what the reference cannot
+    assert P.glynn(big, exact="int128") == 2**124 + 15
+    assert P.ryser(big, exact="int128") == 2**124 + 15
+
+
+def test_cross_algorithm_int_exact(rng):
+    for n in range(1, 8):
+        for m in range(1, n + 1):
+            for _ in range(4):
+                a = rng.integers(0, 10, (m, n)).astype(np.int64)
+                expect = O.brute_force(a.tolist())
+                assert P.combinatoric(a) == expect
+                assert P.ryser(a) == expect
+                assert P.glynn(a) == expect
+                assert P.opt(a) == expect
+
+
+def test_cross_algorithm_float(rng):
+    for n in range(1, 9):
+        for m in range(1, n + 1):
+            a = rng.uniform(-1, 1, (m, n))
+            ref = O.dd_permanent("ryser", a, nthreads=4)
+            M = magsum(a)
+            for fn in (P.combinatoric, P.ryser, P.glynn, P.opt):
+                assert scaled_err(fn(a), ref, M) <= TOL
+            c = a + 1j * rng.uniform(-1, 1, (m, n))
+            ref = O.dd_permanent("ryser", c, nthreads=4)
+            M = magsum(c)
+            for fn in (P.combinatoric, P.ryser, P.glynn, P.opt):
+                assert scaled_err(fn(c), ref, M) <= TOL
+
+
+def test_tall_matrices_transpose(rng):
+    a = rng.uniform(-1, 1, (7, 4))
+    for fn in (P.combinatoric, P.ryser, P.glynn, P.opt):
+        assert fn(a) == pytest.approx(fn(a.T), rel=1e-12)
+
+
+# ---------------------------------------------------- structural properties
+def test_structural_properties(rng):
+    for _ in range(20):
+        n = int(rng.integers(2, 8))
+        m = int(rng.integers(1, n + 1))
+        a = rng.integers(0, 10, (m, n)).astype(np.int64)
+        expect = P.ryser(a)
+        b = a[rng.permutation(m), :][:, rng.permutation(n)]
+        assert P.ryser(b) == expect and P.glynn(b) == expect
+    for _ in range(5):
+        a = rng.uniform(-1, 1, (4, 5))
+        c = float(rng.uniform(0.5, 2.0))
+        s = a.copy()
+        s[2, :] *= c
+        for fn in (P.ryser, P.glynn, P.combinatoric):
+            assert fn(s) == pytest.approx(c * fn(a), rel=1e-12)
+    z = rng.integers(0, 10, (4, 5)).astype(np.int64)
+    z[1, :] = 0
+    assert P.combinatoric(z) == 0 and P.ryser(z) == 0 and P.glynn(z) == 0
+    f = rng.uniform(-1, 1, (4, 5))
+    f[2, :] = 0.0
+    assert P.combinatoric(f) == 0.0 and P.ryser(f) == 0.0 and abs(P.glynn(f)) < 1e-12
+    cz = rng.uniform(-1, 1, (5, 5)) + 1j * rng.uniform(-1, 1, (5, 5))
+    for fn in (P.ryser, P.glynn):
+        assert fn(np.conj(cz)) == pytest.approx(np.conj(fn(cz)), rel=1e-13)
+
+
+def test_device_tensor_input(rng):
+    torch = pytest.importorskip("torch")
+    a = rng.uniform(-1, 1, (14, 14))
+    t = torch.tensor(a, device="cuda")
+    assert P.glynn(t) == pytest.approx(P.glynn(a), rel=1e-13)
+    assert P.ryser(t) == pytest.approx(P.glynn(a), rel=1e-10)
+
+
+# ------------------------------------------------------------- configs C1-C5
+def test_c1_against_reference():
+    """64 x 12x12 U[-1,1]: metric (i) <= 1e-10 against the reference."""
+    d = np.load(GOLDEN / "c1.npz")
+    for a, g, r, o in zip(d["a"], d["glynn"], d["ryser"], d["opt"]):
+        for fn in (P.glynn, P.ryser, P.opt):
+            v = fn(a)
+            assert rel_err(v, g) <= TOL and rel_err(v, r) <= TOL and rel_err(v, o) <= TOL
+
+
+def test_c3a_complex_24():
+    c3 = json.loads((GOLDEN / "c3.json").read_text())
+    a = W.c3a()
+    dd = decode_value(c3["c3a_dd_glynn"])
+    ref_g = decode_value(c3["c3a_ref_glynn"])
+    for fn in (P.glynn, P.ryser):
+        v, M = fn(a), magsum(a)
+        assert scaled_err(v, dd, M) <= TOL
+        assert scaled_err(v, ref_g, M) <= TOL
+    v = P.glynn(a)
+    assert rel_err(v, dd) <= 1e-9  # plain relative error, reported
+
+
+def test_c3b_complex_rectangular():
+    """20x28: the pre-scaled GPU Glynn-rect vs the double-double oracle and
+    the reference's own Glynn on the pre-scaled matrix."""
+    c3 = json.loads((GOLDEN / "c3.json").read_text())
+    b = W.c3b()
+    dd = decode_value(c3["c3b_dd_glynn"])
+    M = magsum(b)
+    for fn in (P.glynn, P.ryser, P.glynn_rectangular):
+        v = fn(b)
+        assert scaled_err(v, dd, M) <= TOL, (fn, v, dd, M)
+    if "c3b_ref_glynn_prescaled" in c3:
+        ref = decode_value(c3["c3b_ref_glynn_prescaled"])
+        assert scaled_err(P.glynn(b), ref, M) <= TOL
+
+
+def test_c4_exact_integer():
+    c4 = json.loads((GOLDEN / "c4.json").read_text())
+    for name, a in (("c4a", W.c4a()), ("c4b", W.c4b())):
+        exact = int(c4[f"{name}_exact"])
+        g = P.glynn(a, exact="int128")
+        r = P.ryser(a, exact="int128")
+        assert g == exact and r == exact
+        if c4[f"{name}_ref"] == "OverflowError":
+            with pytest.raises(OverflowError):
+                P.glynn(a)
+
+
+def test_c4_downscaled_bit_exact():
+    g = np.random.default_rng([2510, 3421, 106])
+    for n in range(12, 20):
+        a = W.bernoulli01(n, g)
+        exact = O.exact_int128("glynn", a)
+        assert P.glynn(a) == exact and P.ryser(a) == exact
+        assert P.glynn(a, exact="int128") == exact
+        b = g.integers(-2, 3, (n, n)).astype(np.int64)
+        exact = O.exact_int128("ryser", b)
+        assert P.ryser(b, exact="int128") == exact == P.glynn(b, exact="int128")
+
+
+def test_c5_closed_forms():
+    a, exact = W.ones(36)
+    v, M = P.permanent_with_magsum(as_matrix(a), AlgorithmId.GLYNN)
+    assert scaled_err(v, exact, M) <= TOL
+    assert rel_err(v, exact) <= 1e-9
+    u, ex = W.rank_one(36)
+    v, M = P.permanent_with_magsum(as_matrix(u), AlgorithmId.GLYNN)
+    assert scaled_err(v, ex, M) <= TOL
+
+
+@pytest.mark.parametrize("n", [20, 22, 24])
+def test_c5_law_downscaled_vs_dd(n):
+    a = W.c5(n)
+    dd = O.dd_permanent("glynn", a)
+    v, M = P.permanent_with_magsum(as_matrix(a), AlgorithmId.GLYNN)
+    assert scaled_err(v, dd, M) <= TOL
+    assert rel_err(v, dd) <= 1e-10
