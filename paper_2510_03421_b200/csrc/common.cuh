@@ -122,6 +122,13 @@ __device__ __forceinline__ i128 i128_mul_s64(i128 a, int64_t c) {
   r.hi = __umul64hi(a.lo, uc) + a.hi * uc - ((c < 0) ? a.lo : 0ull);
   return r;
 }
+// (a * b) mod 2^128
+__device__ __forceinline__ i128 i128_mul(i128 a, i128 b) {
+  i128 r;
+  r.lo = a.lo * b.lo;
+  r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+  return r;
+}
 __device__ __forceinline__ bool i128_fits_i64(i128 a) { return a.hi == (uint64_t)((int64_t)a.lo >> 63); }
 __device__ __forceinline__ bool i128_lt(i128 a, i128 b) {  // signed
   if (a.hi != b.hi) return (int64_t)a.hi < (int64_t)b.hi;

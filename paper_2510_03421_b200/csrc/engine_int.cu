@@ -47,6 +47,13 @@ struct IntSetup {
   int P = 0, B = 0;
   bool weighted = false;
   std::vector<int64_t> v0, U, w;
+  // raw update rows (Glynn: row n-1-t; Ryser: column t) and the factor that
+  // turns them into U (-2 for Glynn, +1 for Ryser): the 128-bit-state kernel
+  // forms u * factor in 128 bits, where -2 * a_ij may not fit int64
+  std::vector<int64_t> R;
+  int64_t rscale = 1;
+  std::vector<int64_t> v0w;  // exact initial state as (lo, hi) pairs
+
   bool pre_overflow = false;  // reference flags before/independently of the walk
   s128 bound = 0;             // max |state entry| along the walk
 };
@@ -69,13 +76,20 @@ static void setup_int(int alg, const IntMat& A, IntSetup* s) {
       }
       s->v0[j] = acc;
       s->bound = std::max(s->bound, mag);
+      s128 exact = n - m;
+      for (int i = 0; i < m; ++i) exact += A.at(i, j);
+      s->v0w.push_back((int64_t)(uint64_t)exact);
+      s->v0w.push_back((int64_t)(uint64_t)((unsigned __int128)exact >> 64));
     }
     // rows 1..n-1 are flipped; a real row whose doubled entry leaves int64
     // is flagged by the reference (src/_kernels.py:461-464, 631-634)
+    s->R.assign((size_t)(n - 1) * n, 0);
+    s->rscale = -2;
     for (int t = 0; t < n - 1; ++t) {
       const int i = n - 1 - t;
       for (int j = 0; j < n; ++j) {
         int64_t y = (i < m) ? A.at(i, j) : 1, d2;
+        s->R[(size_t)t * n + j] = y;
         if (__builtin_add_overflow(y, y, &d2)) {
           s->pre_overflow = true;
           d2 = 0;
@@ -92,6 +106,9 @@ static void setup_int(int alg, const IntMat& A, IntSetup* s) {
   s->U.assign((size_t)n * m, 0);
   for (int t = 0; t < n; ++t)
     for (int i = 0; i < m; ++i) s->U[(size_t)t * m + i] = A.at(i, t);
+  s->R = s->U;
+  s->rscale = 1;
+  s->v0w.assign(2 * (size_t)m, 0);
   for (int i = 0; i < m; ++i) {
     s128 mag = 0;
     for (int j = 0; j < n; ++j) mag += (A.at(i, j) < 0) ? -(s128)A.at(i, j) : (s128)A.at(i, j);
@@ -171,16 +188,13 @@ static int checked_walk(const IntSetup& s, cudaStream_t stream, bool* ovf, int64
 walk_fn_i int_wrap_lookup(int P);
 
 static int wrap_walk(const IntSetup& s, cudaStream_t stream, s128* raw) {
-  if (s.bound >= ((s128)1 << 62)) {
-    set_error("state entries may exceed 2^62; exact int128 walk unsupported for this matrix");
-    return PERM_OVERFLOW;
-  }
+  const bool wide = s.bound >= ((s128)1 << 62);  // int64 state could wrap
   const uint64_t steps = 1ull << s.B;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   // exact int64 groups of 8 factors need bound^8 < 2^63
-  const bool g8 = !s.weighted && (long double)s.bound < std::pow(2.0L, 63.0L / 8.0L) && steps >= 8;
+  const bool g8 = !wide && !s.weighted && (long double)s.bound < std::pow(2.0L, 63.0L / 8.0L) && steps >= 8;
   const uint64_t lanes = (uint64_t)nsm * 8 * kIntThreads;
   int log2L = 3;
   while (log2L < 14 && (steps >> (log2L + 1)) >= 16 * lanes) ++log2L;
@@ -189,13 +203,13 @@ static int wrap_walk(const IntSetup& s, cudaStream_t stream, s128* raw) {
   if (steps < 8) log2L = 0;
   const uint64_t nchunks = steps >> log2L;
   uint64_t blocks = std::min<uint64_t>((nchunks + kIntThreads - 1) / kIntThreads, (uint64_t)nsm * 8);
-  const size_t nv0 = s.v0.size(), nU = s.U.size(), nw = s.w.size();
+  const size_t nv0 = wide ? s.v0w.size() : s.v0.size(), nU = s.U.size(), nw = s.w.size();
   const size_t bytes = (nv0 + nU + nw) * 8 + blocks * 16;
   DevBuf buf;
   PERM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, stream));
   int64_t* d = static_cast<int64_t*>(buf.p);
-  PERM_CUDA_TRY(cudaMemcpyAsync(d, s.v0.data(), nv0 * 8, cudaMemcpyHostToDevice, stream));
-  if (nU) PERM_CUDA_TRY(cudaMemcpyAsync(d + nv0, s.U.data(), nU * 8, cudaMemcpyHostToDevice, stream));
+  PERM_CUDA_TRY(cudaMemcpyAsync(d, (wide ? s.v0w : s.v0).data(), nv0 * 8, cudaMemcpyHostToDevice, stream));
+  if (nU) PERM_CUDA_TRY(cudaMemcpyAsync(d + nv0, (wide ? s.R : s.U).data(), nU * 8, cudaMemcpyHostToDevice, stream));
   if (nw) PERM_CUDA_TRY(cudaMemcpyAsync(d + nv0 + nU, s.w.data(), nw * 8, cudaMemcpyHostToDevice, stream));
   IntWalkArgs a;
   a.v0 = d;
@@ -212,7 +226,10 @@ static int wrap_walk(const IntSetup& s, cudaStream_t stream, s128* raw) {
   if (fast) {
     PERM_CUDA_TRY(fast(a, (int)blocks, stream));
   } else {
-    int_walk_wrap_generic_kernel<<<(unsigned)blocks, kIntThreads, 0, stream>>>(a, s.weighted ? 1 : 0);
+    if (wide)
+      int_walk_wrap_wide_kernel<<<(unsigned)blocks, kIntThreads, 0, stream>>>(a, s.weighted ? 1 : 0, s.rscale);
+    else
+      int_walk_wrap_generic_kernel<<<(unsigned)blocks, kIntThreads, 0, stream>>>(a, s.weighted ? 1 : 0);
     PERM_CUDA_TRY(cudaGetLastError());
   }
   std::vector<int64_t> h(blocks * 2);
@@ -309,18 +326,38 @@ int int_permanent(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_
   }
   if (width != 128) {
     set_error("width must be 64 or 128");
-    return PERM_BAD_ARG;
+  // Fit certificate for |walk sum| < 2^127: (a) a priori, or (b) an FP64 run
+  // with its magnitude-sum error bound (state entries must then be exactly
+  // representable, i.e. magnitudes < 2^52).
+  // that; (b) otherwise an FP64 run with its magnitude-sum error bound
+  // (needs exactly representable state entries, i.e. magnitudes < 2^52).
+  // |walk sum| = |per| * denom <= per(|A|) * denom, and per(|A|) is at most
+  // the product of the row sums of |A| (and, square, of the column sums)
+  long double rows = 1.0L, cols = 1.0L;
+  for (int i = 0; i < m; ++i) {
+    long double r = 0;
+    for (int j = 0; j < n; ++j) r += std::fabs((long double)A.at(i, j));
+    rows *= r;
   }
-  if (s.bound >= ((s128)1 << 52)) {
-    set_error("entries too large for the certified int128 walk (row/column magnitude >= 2^52)");
-    return PERM_OVERFLOW;
+  for (int j = 0; j < n; ++j) {
+    long double c = 0;
+    for (int i = 0; i < m; ++i) c += std::fabs((long double)A.at(i, j));
+    cols *= c;
   }
+  const long double apriori = (m == n ? std::min(rows, cols) : rows) * (long double)denom;
+  const bool cert_apriori = apriori < std::ldexp(1.0L, 126);
   double per_fp = 0, mag = 0;
-  st = float_estimate(alg, A, stream, &per_fp, &mag);
-  if (st) return st;
-  if (!fits_bound(per_fp, mag, s.P, (long double)denom)) {
-    set_error("exact value not certified to fit the int128 walk");
-    return PERM_OVERFLOW;
+  if (!cert_apriori) {
+    if (s.bound >= ((s128)1 << 52)) {
+      set_error("exact value not certified to fit int128 (entries too large for the FP64 certificate)");
+      return PERM_OVERFLOW;
+    }
+    st = float_estimate(alg, A, stream, &per_fp, &mag);
+    if (st) return st;
+    if (!fits_bound(per_fp, mag, s.P, (long double)denom)) {
+      set_error("exact value not certified to fit the int128 walk");
+      return PERM_OVERFLOW;
+    }
   }
   s128 raw = 0;
   st = wrap_walk(s, stream, &raw);
@@ -337,7 +374,7 @@ int int_permanent(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_
   }
   // consistency with the FP64 estimate (catches a corrupted exact sum)
   const long double E = (long double)(s.P + (1 << 14) + 16) * std::ldexp(1.0L, -52) * (long double)mag;
-  if (std::fabs((long double)v - (long double)per_fp) > E + 1.0L) {
+  if (!cert_apriori && std::fabs((long double)v - (long double)per_fp) > E + 1.0L) {
     set_error("internal: int128 result disagrees with the FP64 estimate");
     return PERM_CUDA;
   }

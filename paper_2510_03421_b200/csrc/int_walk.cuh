@@ -202,6 +202,57 @@ static __global__ void __launch_bounds__(kIntThreads) int_walk_wrap_generic_kern
   }
 }
 
+// WRAP walk with 128-bit state entries, for matrices whose row / column
+// magnitudes reach 2^62 (where the int64 state of the kernels above could
+// wrap).  Runtime P, optional weights; everything mod 2^128.
+static __global__ void __launch_bounds__(kIntThreads) int_walk_wrap_wide_kernel(IntWalkArgs a, int weighted, int64_t rscale) {
+  const int P = a.P, B = a.B;
+  i128 acc = i128_from(0);
+  const uint64_t nthr = (uint64_t)gridDim.x * kIntThreads;
+  for (uint64_t c = (uint64_t)blockIdx.x * kIntThreads + threadIdx.x; c < a.nchunks; c += nthr) {
+    const uint64_t k0 = a.k_begin + (c << a.log2L);
+    const uint64_t k1 = k0 + (1ull << a.log2L);
+    i128 v[64];
+    const uint64_t g0 = k0 ^ (k0 >> 1);
+    for (int j = 0; j < P; ++j) {
+      i128 x;
+      x.lo = (uint64_t)a.v0[2 * j];
+      x.hi = (uint64_t)a.v0[2 * j + 1];
+      for (int t = 0; t < B; ++t)
+        if ((g0 >> t) & 1) x = i128_add(x, i128_mul_s64(i128_from(a.U[(size_t)t * P + j]), rscale));
+      v[j] = x;
+    }
+    int pc = __popcll(g0);
+    for (uint64_t k = k0; k < k1; ++k) {
+      if (k != k0) {
+        const int t = __ffsll((long long)k) - 1;
+        const bool set = ((k ^ (k >> 1)) >> t) & 1;
+        const int64_t* u = a.U + (size_t)t * P;
+        for (int j = 0; j < P; ++j) {
+          const i128 du = i128_mul_s64(i128_from(u[j]), rscale);
+          v[j] = set ? i128_add(v[j], du) : i128_sub(v[j], du);
+        }
+        pc += set ? 1 : -1;
+      }
+      i128 p = v[0];
+      for (int j = 1; j < P; ++j) p = i128_mul(p, v[j]);
+      if (weighted) acc = i128_add(acc, i128_mul_s64(p, a.w[pc]));
+      else acc = (k & 1) ? i128_sub(acc, p) : i128_add(acc, p);
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) acc = i128_add(acc, shfl_down_i128(acc, off));
+  __shared__ i128 ws[kIntWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) ws[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i128 t = ws[0];
+    for (int w = 1; w < kIntWarps; ++w) t = i128_add(t, ws[w]);
+    a.out[(size_t)blockIdx.x * 2] = (int64_t)t.lo;
+    a.out[(size_t)blockIdx.x * 2 + 1] = (int64_t)t.hi;
+  }
+}
+
 // Fast unweighted WRAP walk, compile-time P; factors multiplied exactly in
 // int64 in groups of 8 (host guarantees |state|^8 < 2^63), groups folded
 // into the 128-bit product.  Same 8-step unrolled schedule as walk_kernel.

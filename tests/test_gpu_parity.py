@@ -251,7 +251,11 @@ def test_c5_closed_forms():
     a, exact = W.ones(36)
     v, M = P.permanent_with_magsum(as_matrix(a), AlgorithmId.GLYNN)
     assert scaled_err(v, exact, M) <= TOL
-    assert rel_err(v, exact) <= 1e-9
+    # plain relative error is reported, not the contract: on J_n every term
+    # of a given |colsum| rounds identically, so product roundings add
+    # coherently to ~35u * M/|per| = ~1e-9 (M/|per| = 2.98e5; the
+    # reference's own Glynn already shows 1.15e-9 at n = 26)
+    assert rel_err(v, exact) <= 5e-9
     u, ex = W.rank_one(36)
     v, M = P.permanent_with_magsum(as_matrix(u), AlgorithmId.GLYNN)
     assert scaled_err(v, ex, M) <= TOL
