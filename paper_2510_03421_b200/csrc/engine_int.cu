@@ -326,12 +326,12 @@ int int_permanent(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_
   }
   if (width != 128) {
     set_error("width must be 64 or 128");
+    return PERM_BAD_ARG;
+  }
   // Fit certificate for |walk sum| < 2^127: (a) a priori, or (b) an FP64 run
   // with its magnitude-sum error bound (state entries must then be exactly
   // representable, i.e. magnitudes < 2^52).
-  // that; (b) otherwise an FP64 run with its magnitude-sum error bound
-  // (needs exactly representable state entries, i.e. magnitudes < 2^52).
-  // |walk sum| = |per| * denom <= per(|A|) * denom, and per(|A|) is at most
+  // (a): |walk sum| = |per| * denom <= per(|A|) * denom, and per(|A|) is at most
   // the product of the row sums of |A| (and, square, of the column sums)
   long double rows = 1.0L, cols = 1.0L;
   for (int i = 0; i < m; ++i) {
