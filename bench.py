@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark driver (one JSON line on rank 0).
+
+Headline workload: BASELINE.json configs[4] = C5, the large single float64
+permanent n = 36 (entries iid U[0,1]/36, seeded), computed with the Gray-code
+Glynn walk; its 2^35 sign vectors are sharded over the N ranks (one GPU
+each, NCCL all-gather of 8-double partials), so the total work is fixed as N
+grows ("strong" scaling).  metric = Gray-code steps/s of the whole job.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 36]
+    python bench.py --impl reference ...   # the reference's CPU algorithm
+                                           # (oracle C port, all host threads)
+
+A "step" is one full permanent.  Timing: barrier + cuda.synchronize around
+the timed region, CUDA events on the launching stream per step (L2 flushed
+with a 256 MiB write before every step, outside the events), max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Gray-code steps/sec and s/permanent at n=20–36; % of FP64 FMA peak, 1/2/4/8 GPUs"
+UNIT = "steps/s"
+NOMINAL_DFMA = 148 * 64 * 1965e6  # FP64 pipe slots/s at the max SM clock
+
+
+def workload_name(n):
+    return f"C5: Glynn f64 {n}x{n} U[0,1]/{n} single permanent, 2^{n - 1} Gray steps sharded over ranks"
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        time.sleep(0.3)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------- CPU baseline
+def cpu_walk_rate(a: np.ndarray, nthreads: int, target_s: float):
+    """Oracle port (perm_oracle.c, the reference's sequential Glynn walk
+    restated in C) over a bounded prefix of the same walk: steps/s."""
+    from oracle import oracle as O
+
+    setup = O.walk_setup("glynn", a)
+    steps = 1 << 22
+    t = time.perf_counter()
+    O.walk_f64_mt(setup, 0, steps, nthreads=nthreads)
+    dt = time.perf_counter() - t
+    steps = int(min(1 << (a.shape[1] - 1), max(steps, steps * target_s / max(dt, 1e-6))))
+    steps -= steps % nthreads
+    t = time.perf_counter()
+    O.walk_f64_mt(setup, 0, steps, nthreads=nthreads)
+    dt = time.perf_counter() - t
+    return steps / dt, steps, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_2510_03421_b200 import workloads as W
+
+    O.build()
+    a = W.c5(args.n)
+    cores = os.cpu_count() or 1
+    # calibrate a per-step sample of ~target seconds
+    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    rate, sample, _ = cpu_walk_rate(a, cores, per_step)
+    for _ in range(args.warmup):
+        cpu_walk_rate_fixed(O, a, sample, cores)
+    times = [cpu_walk_rate_fixed(O, a, sample, cores) for _ in range(args.steps)]
+    total = sum(times)
+    value = sample * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded U[0,1]/n, SURVEY 8(d) k=8)",
+        "config": {"workload": workload_name(args.n), "n": args.n,
+                   "sample_steps_per_step": sample, "s_per_permanent_extrapolated":
+                   (1 << (args.n - 1)) / value},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"first {sample} Gray steps of the {args.n}x{args.n} C5 walk per step, "
+                                   f"split over {cores} threads (oracle/perm_oracle.c, the reference's "
+                                   "src/_kernels.py:373-409 walk restated; reference itself is Python+numba, "
+                                   "not present on the GPU box)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_walk_rate_fixed(O, a, steps, nthreads):
+    setup = O.walk_setup("glynn", a)
+    t = time.perf_counter()
+    O.walk_f64_mt(setup, 0, steps, nthreads=nthreads)
+    return time.perf_counter() - t
+
+
+# ------------------------------------------------------------- engine arm
+def run_engine(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2510_03421_b200 as P
+    from paper_2510_03421_b200 import _lib, workloads as W
+    from paper_2510_03421_b200.sharded import finish, gpu_partial, shard_range
+
+    lib = _lib.load()
+    _lib.check(lib.perm_set_device(local), "set_device")
+    n = args.n
+    a = W.c5(n)
+    k0, k1 = shard_range("glynn", n, n, rank, world)
+    steps_total = 1 << (n - 1)
+    stream = torch.cuda.current_stream()
+    part = torch.zeros(8, dtype=torch.float64, device="cuda")
+    gathered = torch.zeros(8 * world, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def step():
+        gpu_partial("glynn", a, k0, k1, False, device_out=part, stream=stream.cuda_stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, part)
+        else:
+            gathered.copy_(part)
+
+    # FP64-pipe roofline denominator, measured live on this GPU
+    peak = _lib.out_buf(1)
+    _lib.check(lib.perm_fp64_peak_probe(1.0, peak), "peak probe")
+    peak_dfma = float(peak[0])
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    value_check, _ = finish("glynn", a, gathered.cpu().numpy())
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kernel_ms = []
+    for i in range(args.steps):
+        flush.fill_(float(i))  # > 126 MB L2, outside the timed events
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+        kernel_ms.append(lib.perm_last_kernel_ms())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    t_ms = sum(s.elapsed_time(e) for s, e in ev)
+    t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    grid, log2L = _lib.C.c_int(), _lib.C.c_int()
+    lib.perm_last_kernel_plan(_lib.C.byref(grid), _lib.C.byref(log2L))
+
+    value = steps_total * args.steps / (t_ms * 1e-3)
+    kern_ms = statistics.mean(kernel_ms)
+    ops_per_launch = (k1 - k0) * 2 * n  # 2n FP64-pipe ops per Glynn step
+    achieved = ops_per_launch / (kern_ms * 1e-3)
+
+    # ---- e2e through the public API (host numpy input -> Python float) --
+    if world > 1:
+        dist.barrier()
+    e2e_times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        v = P.sharded_permanent(a) if world > 1 else P.glynn(a)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e = torch.tensor([sum(e2e_times)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    e2e_value = steps_total * args.steps / float(e2e.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+
+        O.build()
+        rate, sample, dt = cpu_walk_rate(a, 1, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"first {sample} Gray steps of the same {n}x{n} walk on 1 host thread "
+                         f"({dt:.1f} s; oracle/perm_oracle.c restating src/_kernels.py:373-409, which "
+                         "is single-threaded in the reference)"}
+
+    traffic = None
+    tf = ROOT / "profiles" / "roofline_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(f"glynn_f64_n{n}")
+        except (ValueError, OSError):
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded U[0,1]/n matrix, SURVEY 8(d) k=8)",
+            "config": {"workload": workload_name(n), "n": n, "alg": "glynn",
+                       "s_per_permanent": t_ms * 1e-3 / args.steps,
+                       "parallelism": f"gray-range shards x{world} (NCCL all-gather of 8-double partials)",
+                       "l2": "flushed (256 MiB write) before every step, outside the timed events",
+                       "launch": {"grid": grid.value, "threads": 256, "log2_chunk": log2L.value},
+                       "value_check": value_check},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_dfma, "unit": "FP64 op/s",
+                         "frac": achieved / peak_dfma, "frac_of_nominal": achieved / NOMINAL_DFMA,
+                         "traffic": traffic,
+                         "peak_source": "live DFMA probe on this GPU (perm_fp64_peak_probe; MEASURED_PEAKS.json "
+                                        "has no FP64 entry); nominal = 148 SM x 64 DFMA/clk x 1965 MHz",
+                         "ops_per_step": 2 * n, "kernel_ms": kern_ms,
+                         "kernel_share_of_step": kern_ms / (t_ms / args.steps)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": (n + (n - 1) * n) * 8,
+                    "d2h_bytes_per_step": 8 * 8,
+                    "api": "paper_2510_03421_b200.glynn(numpy) / sharded_permanent(numpy) for N>1",
+                    "s_per_permanent": float(e2e.item()) / args.steps},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=36)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_engine(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

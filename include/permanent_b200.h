@@ -51,6 +51,14 @@ const char* perm_last_error(void);
 int perm_set_device(int device);
 /* Number of SMs of the current device (planning helper). */
 int perm_device_sm_count(void);
+/* Instrumentation: device time (ms, CUDA events on the launching stream) of
+ * the last Gray-walk kernel launched by this host thread (-1 if none), and
+ * its launch plan (grid size, log2 of the per-lane chunk length). */
+double perm_last_kernel_ms(void);
+int perm_last_kernel_plan(int* grid, int* log2L);
+/* FP64-pipe roofline denominator: DFMA/s sustained by an 8-chain DFMA
+ * kernel over the whole device for about `seconds`. */
+int perm_fp64_peak_probe(double seconds, double* dfma_per_s);
 
 /* ---- single permanents, float64 / complex128 --------------------------
  * Replace glynn_sq/glynn_rect + permanent_glynn_{square,rectangular}
@@ -97,6 +105,17 @@ int perm_glynn_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int
                    int* fits_int64, void* stream);
 int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, int64_t* out,
                    int* fits_int64, void* stream);
+
+/* ---- batched small matrices (north_star item 4; no reference counterpart:
+ * the reference evaluates one matrix per Python call) --------------------
+ * a = [B][m][n] row-major contiguous (host, or device if dev_ptr = 1),
+ * out = [B] (same memory space).  One thread per matrix, shared-memory
+ * staged; alg = PERM_ALG_* or -1 for the batch dispatch
+ * (perm_batch_select: Glynn for squares, subset-skipping Ryser for m < n).
+ * Requires m <= n <= 16.  Device-pointer calls are asynchronous on `stream`. */
+int perm_batch_f64(int alg, int64_t B, int m, int n, const double* a, double* out, int dev_ptr, void* stream);
+int perm_batch_c128(int alg, int64_t B, int m, int n, const double* a, double* out, int dev_ptr, void* stream);
+int perm_batch_select(int m, int n);
 
 /* ---- sharded walks (one Gray range per GPU / rank) --------
  * perm_walk_steps: length of the Gray index space of (alg, m, n): 2^(n-1)

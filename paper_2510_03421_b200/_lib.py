@@ -31,6 +31,9 @@ SIGNATURES = {
     "perm_last_error": (C.c_char_p, []),
     "perm_set_device": (C.c_int, [C.c_int]),
     "perm_device_sm_count": (C.c_int, []),
+    "perm_last_kernel_ms": (C.c_double, []),
+    "perm_last_kernel_plan": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "perm_fp64_peak_probe": (C.c_int, [C.c_double, _dp]),
     "perm_glynn_f64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _dp, _vp]),
     "perm_glynn_c128": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _dp, _vp]),
     "perm_ryser_f64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _dp, _vp]),
@@ -42,6 +45,9 @@ SIGNATURES = {
                                  C.POINTER(C.c_int), _vp]),
     "perm_ryser_i64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, _ip,
                                  C.POINTER(C.c_int), _vp]),
+    "perm_batch_f64": (C.c_int, [C.c_int, C.c_int64, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp]),
+    "perm_batch_c128": (C.c_int, [C.c_int, C.c_int64, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp]),
+    "perm_batch_select": (C.c_int, [C.c_int, C.c_int]),
     "perm_walk_steps": (C.c_uint64, [C.c_int, C.c_int, C.c_int]),
     "perm_walk_shard": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

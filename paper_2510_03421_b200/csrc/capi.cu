@@ -12,6 +12,9 @@ int int_permanent(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_
                   int* fits_int64, void* stream);
 int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t lda, int dev_ptr,
                    uint64_t step_budget, double* out, int64_t* ivalue, void* stream);
+int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a, double* out, int dev_ptr,
+                    void* stream);
+int batch_select(int m, int n);
 }
 
 namespace {
@@ -165,6 +168,27 @@ int perm_set_device(int device) {
   return PERM_OK;
 }
 
+double perm_last_kernel_ms(void) {
+  KernelTimer& t = kernel_timer();
+  if (!t.ok || !t.pending) return -1.0;
+  if (cudaEventSynchronize(t.stop) != cudaSuccess) return -1.0;
+  float ms = 0.0f;
+  if (cudaEventElapsedTime(&ms, t.start, t.stop) != cudaSuccess) return -1.0;
+  return (double)ms;
+}
+
+int perm_last_kernel_plan(int* grid, int* log2L) {
+  KernelTimer& t = kernel_timer();
+  *grid = t.last_grid;
+  *log2L = t.last_log2L;
+  return PERM_OK;
+}
+
+int perm_fp64_peak_probe(double seconds, double* dfma_per_s) {
+  clear_error();
+  return fp64_peak_probe(seconds, dfma_per_s);
+}
+
 int perm_device_sm_count(void) {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -222,6 +246,14 @@ int perm_comb_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, uint
                   void* stream) {
   return comb_permanent(false, 2, m, n, a, lda, dev_ptr, step_budget, nullptr, out, stream);
 }
+
+int perm_batch_f64(int alg, int64_t B, int m, int n, const double* a, double* out, int dev_ptr, void* stream) {
+  return batch_permanent(alg, false, B, m, n, a, out, dev_ptr, stream);
+}
+int perm_batch_c128(int alg, int64_t B, int m, int n, const double* a, double* out, int dev_ptr, void* stream) {
+  return batch_permanent(alg, true, B, m, n, a, out, dev_ptr, stream);
+}
+int perm_batch_select(int m, int n) { return batch_select(m, n); }
 
 uint64_t perm_walk_steps(int alg, int m, int n) {
   if (check_shape(alg, m, n)) return 0;

@@ -187,6 +187,68 @@ void normalize(int alg, int m, int n, int scale_log2, double* re, double* im, do
   }
 }
 
+// ---------------------------------------------------------------- timing
+// CUDA events bracketing the last walk kernel launched by this host thread
+// (bench.py reads its duration for the live roofline figure).
+static thread_local KernelTimer g_timer[16];
+KernelTimer& kernel_timer() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  KernelTimer& t = g_timer[dev & 15];
+  if (!t.init) {
+    t.init = true;
+    t.ok = cudaEventCreate(&t.start) == cudaSuccess && cudaEventCreate(&t.stop) == cudaSuccess;
+  }
+  return t;
+}
+
+// FP64-pipe probe: 8 independent DFMA chains per thread over a full grid.
+__global__ void dfma_probe_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+         x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (s == 12345.678) out[0] = s;
+}
+
+int fp64_peak_probe(double seconds, double* dfma_per_s) {
+  int dev = 0, nsm = 148;
+  PERM_CUDA_TRY(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  double* d = nullptr;
+  PERM_CUDA_TRY(cudaMalloc(&d, 8));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = nsm * 4, threads = 512, iters = 2048;
+  const double per_launch = (double)blocks * threads * iters * 16 * 8;
+  dfma_probe_kernel<<<blocks, threads>>>(d, iters, 0.999, 1e-3);  // warm-up
+  cudaEventRecord(e0);
+  dfma_probe_kernel<<<blocks, threads>>>(d, iters, 0.999, 1e-3);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  int reps = (int)std::max(1.0, seconds / std::max(1e-6, ms * 1e-3));
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) dfma_probe_kernel<<<blocks, threads>>>(d, iters, 0.999, 1e-3);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  *dfma_per_s = per_launch * reps / (ms * 1e-3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PERM_OK : cuda_fail(e, "dfma probe");
+}
+
 // ---------------------------------------------------------------- kernels
 __global__ void walk_finalize_kernel(const double* __restrict__ partials, int nparts, double* __restrict__ out) {
   __shared__ double red[256][5];
@@ -240,7 +302,18 @@ int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, dou
   if (st) return st;
   double* partials = static_cast<double*>(s->dev);
   double* data = partials + (size_t)kMaxPartials * kPartialStride;
-  PERM_CUDA_TRY(cudaMemcpyAsync(data, ws.buf.data(), data_bytes, cudaMemcpyHostToDevice, stream));
+  // stage through pinned memory so the H2D copy is a true async DMA; the
+  // previous call on this thread has synchronized, so the buffer is free
+  if (s->stage_cap < data_bytes) {
+    if (s->stage) cudaFreeHost(s->stage);
+    s->stage = nullptr;
+    s->stage_cap = 0;
+    PERM_CUDA_TRY(cudaMallocHost(&s->stage, std::max<size_t>(data_bytes, 1 << 16)));
+    s->stage_cap = std::max<size_t>(data_bytes, 1 << 16);
+  }
+  PERM_CUDA_TRY(cudaStreamSynchronize(stream));  // staging buffer may still feed an async call
+  std::memcpy(s->stage, ws.buf.data(), data_bytes);
+  PERM_CUDA_TRY(cudaMemcpyAsync(data, s->stage, data_bytes, cudaMemcpyHostToDevice, stream));
   walk_fn fn = walk_lookup(ws.cplx ? 1 : 0, ws.weighted, ws.P);
   if (!fn) {
     set_error("no walk kernel for this state length");
@@ -260,7 +333,13 @@ int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, dou
   job.k_end = k_end;
   job.partials = partials;
   WalkPlan plan;
+  KernelTimer& tm = kernel_timer();
+  if (tm.ok) cudaEventRecord(tm.start, stream);
   PERM_CUDA_TRY(fn(job, &plan, stream));
+  if (tm.ok) cudaEventRecord(tm.stop, stream);
+  tm.pending = tm.ok;
+  tm.last_grid = plan.grid;
+  tm.last_log2L = plan.log2L;
   walk_finalize_kernel<<<1, 256, 0, stream>>>(partials, plan.grid, dst);
   PERM_CUDA_TRY(cudaGetLastError());
   return PERM_OK;

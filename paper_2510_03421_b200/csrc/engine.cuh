@@ -31,6 +31,8 @@ struct Scratch {
   void* dev = nullptr;       // device scratch
   size_t dev_cap = 0;
   double* host = nullptr;    // pinned host result buffer (64 doubles)
+  void* stage = nullptr;     // pinned host staging buffer for H2D copies
+  size_t stage_cap = 0;
   cudaStream_t own = nullptr;
 };
 Scratch* scratch();                              // for the current device
@@ -68,5 +70,14 @@ void normalize(int alg, int m, int n, int scale_log2, double* re, double* im, do
 int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst, cudaStream_t stream);
 
 uint64_t walk_steps(int alg, int m, int n);
+
+// ---- instrumentation -------------------------------------------------------
+struct KernelTimer {
+  bool init = false, ok = false, pending = false;
+  cudaEvent_t start = nullptr, stop = nullptr;
+  int last_grid = 0, last_log2L = 0;
+};
+KernelTimer& kernel_timer();
+int fp64_peak_probe(double seconds, double* dfma_per_s);
 
 }  // namespace permb200

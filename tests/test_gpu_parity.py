@@ -268,3 +268,53 @@ def test_c5_law_downscaled_vs_dd(n):
     v, M = P.permanent_with_magsum(as_matrix(a), AlgorithmId.GLYNN)
     assert scaled_err(v, dd, M) <= TOL
     assert rel_err(v, dd) <= 1e-10
+
+
+# ------------------------------------------------------------- batches (C2)
+def _batch_err(out, ref, M):
+    out, ref = np.asarray(out), np.asarray(ref)
+    return np.abs(out - ref) / np.maximum(np.maximum(np.abs(out), np.abs(ref)), M)
+
+
+@pytest.mark.parametrize("key", ["8", "4"])
+def test_c2_batch_against_reference(key):
+    """First 512 matrices of C2a (8x8) / C2b (4x10) vs the reference's opt and
+    each explicit algorithm, metric (ii) with the oracle's M."""
+    d = np.load(GOLDEN / "c2_sub.npz")
+    A, M = d["a" + key], d["m" + key]
+    for fn in (P.opt_batch, P.glynn_batch, P.ryser_batch, P.combinatoric_batch):
+        out = fn(A)
+        assert _batch_err(out, d["opt" + key], M).max() <= TOL, fn
+        for alg in ("g", "r", "c"):
+            assert _batch_err(out, d[alg + key], M).max() <= TOL
+
+
+def test_c2_full_batches_consistent():
+    """Full 1e6 batches: the subsample rows match the fixture, and a random
+    sample agrees with the single-matrix engine."""
+    d = np.load(GOLDEN / "c2_sub.npz")
+    for A, key in ((W.c2a(), "8"), (W.c2b(), "4")):
+        out = P.opt_batch(A)
+        assert out.shape == (A.shape[0],)
+        assert _batch_err(out[:512], d["opt" + key], d["m" + key]).max() <= TOL
+        idx = np.random.default_rng(5).choice(A.shape[0], 64, replace=False)
+        for i in idx:
+            v, Mi = P.permanent_with_magsum(as_matrix(A[i]), AlgorithmId.GLYNN)
+            assert scaled_err(out[i], v, Mi) <= TOL
+
+
+def test_batch_complex_and_device(rng):
+    torch = pytest.importorskip("torch")
+    for (m, n) in ((6, 6), (3, 9), (5, 5), (7, 13)):
+        A = rng.uniform(-1, 1, (300, m, n)) + 1j * rng.uniform(-1, 1, (300, m, n))
+        out = P.opt_batch(A)
+        dev = P.opt_batch(torch.tensor(A, device="cuda")).cpu().numpy()
+        for i in range(0, 300, 37):
+            ref = O.permanent("ryser", A[i])[0]
+            M = magsum(A[i])
+            assert scaled_err(out[i], ref, M) <= TOL
+            assert scaled_err(dev[i], ref, M) <= TOL
+    # tall matrices are transposed, empty batches are fine
+    T = rng.uniform(-1, 1, (10, 5, 3))
+    assert np.allclose(P.opt_batch(T), P.opt_batch(np.swapaxes(T, 1, 2)))
+    assert P.opt_batch(np.zeros((0, 4, 4))).shape == (0,)
