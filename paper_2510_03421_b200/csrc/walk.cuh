@@ -51,30 +51,53 @@ struct WalkArgs {
   double* partials;      // [gridDim.x][kPartialStride]
 };
 
-// Shared-memory reads of U rows are volatile on purpose: with plain loads
-// ptxas hoists every row read of the 8 unrolled steps to the top of the block
-// (the rows are loop-invariant), keeping ~8 rows live and spilling at P >= 20.
-// A warp-uniform read is a single broadcast wavefront, so re-reading is cheap.
+// Shared-memory reads of U rows go through `asm volatile` 128-bit loads on
+// purpose: with plain loads NVVM hoists every row read of the 8 unrolled
+// steps to the top of the block (the rows are loop-invariant), keeping ~8
+// rows live and spilling at P >= 20; C++ `volatile` stops that but splits
+// each pair into two LDS.64, which saturated the LSU pipe (ncu: 85% LSU next
+// to 86% FP64).  One LDS.128 per pair of doubles / per complex element, and
+// a warp-uniform address is a single broadcast wavefront.
+#ifndef WALK_LDS
+#define WALK_LDS 1
+#endif
+__device__ __forceinline__ double2 lds2(const void* p) {
+#if WALK_LDS == 0
+  const volatile double* q = static_cast<const volatile double*>(p);
+  double2 r;
+  r.x = q[0];
+  r.y = q[1];
+  return r;
+#else
+  double2 r;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(a));
+  return r;
+#endif
+}
+__device__ __forceinline__ double lds1(const void* p) {
+  double r;
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(p));
+  asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(r) : "r"(a));
+  return r;
+}
+
 template <typename T>
 __device__ __forceinline__ T ld_row(const T* row, int j) {
   if constexpr (sizeof(T) == 16) {
-    const volatile double2* p = reinterpret_cast<const volatile double2*>(row) + j;
-    double2 u;
-    u.x = p->x;
-    u.y = p->y;
+    const double2 u = lds2(row + j);
     return cd_make(u.x, u.y);
   } else {
-    return reinterpret_cast<const volatile double*>(row)[j];
+    return lds1(row + j);
   }
 }
 
 template <typename T, int P>
 __device__ __forceinline__ void row_add(T (&v)[P], const T* __restrict__ row) {
   if constexpr (sizeof(T) == 8 && P >= 2) {
-    const volatile double2* r2 = reinterpret_cast<const volatile double2*>(row);
 #pragma unroll
     for (int j = 0; j < P / 2; ++j) {
-      double2 u; u.x = r2[j].x; u.y = r2[j].y;
+      const double2 u = lds2(row + 2 * j);
       v[2 * j] = Num<T>::add(v[2 * j], u.x);
       v[2 * j + 1] = Num<T>::add(v[2 * j + 1], u.y);
     }
@@ -88,10 +111,9 @@ __device__ __forceinline__ void row_add(T (&v)[P], const T* __restrict__ row) {
 template <typename T, int P>
 __device__ __forceinline__ void row_sub(T (&v)[P], const T* __restrict__ row) {
   if constexpr (sizeof(T) == 8 && P >= 2) {
-    const volatile double2* r2 = reinterpret_cast<const volatile double2*>(row);
 #pragma unroll
     for (int j = 0; j < P / 2; ++j) {
-      double2 u; u.x = r2[j].x; u.y = r2[j].y;
+      const double2 u = lds2(row + 2 * j);
       v[2 * j] = Num<T>::sub(v[2 * j], u.x);
       v[2 * j + 1] = Num<T>::sub(v[2 * j + 1], u.y);
     }
@@ -105,10 +127,9 @@ __device__ __forceinline__ void row_sub(T (&v)[P], const T* __restrict__ row) {
 template <typename T, int P>
 __device__ __forceinline__ void row_fma(T (&v)[P], double s, const T* __restrict__ row) {
   if constexpr (sizeof(T) == 8 && P >= 2) {
-    const volatile double2* r2 = reinterpret_cast<const volatile double2*>(row);
 #pragma unroll
     for (int j = 0; j < P / 2; ++j) {
-      double2 u; u.x = r2[j].x; u.y = r2[j].y;
+      const double2 u = lds2(row + 2 * j);
       v[2 * j] = Num<T>::fmas(s, u.x, v[2 * j]);
       v[2 * j + 1] = Num<T>::fmas(s, u.y, v[2 * j + 1]);
     }
@@ -127,7 +148,23 @@ __host__ __device__ constexpr int row_stride() { return (sizeof(T) == 8) ? ((P +
 // Product of the state vector with kChains interleaved multiply chains: depth
 // P/kChains, only kChains temporaries live (a full pairwise tree keeps P/2
 // extra values live and spills at P >= 20).
-constexpr int kChains = 4;
+#ifndef WALK_CHAINS
+#define WALK_CHAINS 8
+#endif
+constexpr int kChains = WALK_CHAINS;
+template <typename T, int N>
+__device__ __forceinline__ T tree_of(const T (&c)[N]) {
+  if constexpr (N == 1) {
+    return c[0];
+  } else {
+    constexpr int H = (N + 1) / 2;
+    T t[H];
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) t[i] = Num<T>::mul(c[2 * i], c[2 * i + 1]);
+    if constexpr (N & 1) t[H - 1] = c[N - 1];
+    return tree_of<T, H>(t);
+  }
+}
 template <typename T, int P>
 __device__ __forceinline__ T chain_product(const T (&v)[P]) {
   constexpr int C = (P < kChains) ? P : kChains;
@@ -136,10 +173,7 @@ __device__ __forceinline__ T chain_product(const T (&v)[P]) {
   for (int i = 0; i < C; ++i) c[i] = v[i];
 #pragma unroll
   for (int j = C; j < P; ++j) c[j % C] = Num<T>::mul(c[j % C], v[j]);
-  if constexpr (C == 1) return c[0];
-  else if constexpr (C == 2) return Num<T>::mul(c[0], c[1]);
-  else if constexpr (C == 3) return Num<T>::mul(Num<T>::mul(c[0], c[1]), c[2]);
-  else return Num<T>::mul(Num<T>::mul(c[0], c[1]), Num<T>::mul(c[2], c[3]));
+  return tree_of<T, C>(c);
 }
 
 // Occupancy target: cap registers so at least 16 warps per SM stay resident
@@ -150,22 +184,69 @@ __host__ __device__ constexpr int walk_min_blocks() {
   return (Num<T>::kDoubles == 1) ? ((P <= 20) ? 3 : (P <= 44) ? 2 : 1) : ((P <= 14) ? 2 : 1);
 }
 
-template <typename T, int P, bool W>
+template <typename T, int P, bool W, bool MAG>
 struct Term {
   // chunk sum, magnitude sum
   __device__ __forceinline__ static void add(const T (&v)[P], int sign, int pc, const double* sW, T& acc,
-                                             double& mag, int mag_on) {
+                                             double& mag) {
     T p = chain_product<T, P>(v);
     if constexpr (W) {
       double wt = sW[pc];
       acc = Num<T>::add(acc, Num<T>::scale(wt, p));
-      if (mag_on) mag += fabs(wt) * Num<T>::absval(p);
+      if constexpr (MAG) mag += fabs(wt) * Num<T>::absval(p);
     } else {
       acc = (sign > 0) ? Num<T>::add(acc, p) : Num<T>::sub(acc, p);
-      if (mag_on) mag += Num<T>::absval(p);
+      if constexpr (MAG) mag += Num<T>::absval(p);
     }
   }
 };
+
+// The 8-step unrolled walk over one chunk of nq*8 indices starting at k0
+// (state v already seeded): every flip row but one per 8 steps is a
+// compile-time row of U (t = 0, 1, 0, 2, 0, 1, 0).
+template <typename T, int P, bool W, bool MAG>
+__device__ __forceinline__ T walk_chunk(T (&v)[P], const T* sU, const double* sW, uint64_t k0, uint64_t nq, int pc,
+                                        double& mag) {
+  constexpr int PS = row_stride<T, P>();
+  using Tm = Term<T, P, W, MAG>;
+  T acc = Num<T>::zero();
+  for (uint64_t q = 0; q < nq; ++q) {
+    const uint64_t l0 = q << 3;
+    if (q) {
+      const int t = __ffsll((long long)l0) - 1;
+      const uint64_t k = k0 + l0;
+      const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
+      row_fma<T, P>(v, set ? 1.0 : -1.0, sU + t * PS);
+      if constexpr (W) pc += set ? 1 : -1;
+    }
+    Tm::add(v, +1, pc, sW, acc, mag);
+    row_add<T, P>(v, sU);  // l = 1: bit 0 set
+    if constexpr (W) ++pc;
+    Tm::add(v, -1, pc, sW, acc, mag);
+    row_add<T, P>(v, sU + PS);  // l = 2: bit 1 set
+    if constexpr (W) ++pc;
+    Tm::add(v, +1, pc, sW, acc, mag);
+    row_sub<T, P>(v, sU);  // l = 3: bit 0 cleared
+    if constexpr (W) --pc;
+    Tm::add(v, -1, pc, sW, acc, mag);
+    {  // l = 4: bit 2 toggles; set iff bit 3 of (k0 + l0) is clear
+      const int b3 = (int)(((k0 + l0) >> 3) & 1);
+      row_fma<T, P>(v, b3 ? -1.0 : 1.0, sU + 2 * PS);
+      if constexpr (W) pc += b3 ? -1 : 1;
+    }
+    Tm::add(v, +1, pc, sW, acc, mag);
+    row_add<T, P>(v, sU);  // l = 5: bit 0 set
+    if constexpr (W) ++pc;
+    Tm::add(v, -1, pc, sW, acc, mag);
+    row_sub<T, P>(v, sU + PS);  // l = 6: bit 1 cleared
+    if constexpr (W) --pc;
+    Tm::add(v, +1, pc, sW, acc, mag);
+    row_sub<T, P>(v, sU);  // l = 7: bit 0 cleared
+    if constexpr (W) --pc;
+    Tm::add(v, -1, pc, sW, acc, mag);
+  }
+  return acc;
+}
 
 template <typename T, int P, bool W>
 __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_kernel(WalkArgs args) {
@@ -232,44 +313,9 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_ke
         row_fma<T, P>(v, s, sU + b * PS);
       }
     }
-    int pc = __popcll(g0);
-
-    T acc = Num<T>::zero();
-    for (uint64_t q = 0; q < nq; ++q) {
-      const uint64_t l0 = q << 3;
-      if (q) {
-        const int t = __ffsll((long long)l0) - 1;
-        const uint64_t k = k0 + l0;
-        const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
-        row_fma<T, P>(v, set ? 1.0 : -1.0, sU + t * PS);
-        if constexpr (W) pc += set ? 1 : -1;
-      }
-      Term<T, P, W>::add(v, +1, pc, sW, acc, mag, mag_on);
-      row_add<T, P>(v, sU);  // l = 1: bit 0 set
-      if constexpr (W) ++pc;
-      Term<T, P, W>::add(v, -1, pc, sW, acc, mag, mag_on);
-      row_add<T, P>(v, sU + PS);  // l = 2: bit 1 set
-      if constexpr (W) ++pc;
-      Term<T, P, W>::add(v, +1, pc, sW, acc, mag, mag_on);
-      row_sub<T, P>(v, sU);  // l = 3: bit 0 cleared
-      if constexpr (W) --pc;
-      Term<T, P, W>::add(v, -1, pc, sW, acc, mag, mag_on);
-      {  // l = 4: bit 2 toggles; set iff bit 3 of (k0 + l0) is clear
-        const int b3 = (int)(((k0 + l0) >> 3) & 1);
-        row_fma<T, P>(v, b3 ? -1.0 : 1.0, sU + 2 * PS);
-        if constexpr (W) pc += b3 ? -1 : 1;
-      }
-      Term<T, P, W>::add(v, +1, pc, sW, acc, mag, mag_on);
-      row_add<T, P>(v, sU);  // l = 5: bit 0 set
-      if constexpr (W) ++pc;
-      Term<T, P, W>::add(v, -1, pc, sW, acc, mag, mag_on);
-      row_sub<T, P>(v, sU + PS);  // l = 6: bit 1 cleared
-      if constexpr (W) --pc;
-      Term<T, P, W>::add(v, +1, pc, sW, acc, mag, mag_on);
-      row_sub<T, P>(v, sU);  // l = 7: bit 0 cleared
-      if constexpr (W) --pc;
-      Term<T, P, W>::add(v, -1, pc, sW, acc, mag, mag_on);
-    }
+    const int pc = __popcll(g0);
+    const T acc = mag_on ? walk_chunk<T, P, W, true>(v, sU, sW, k0, nq, pc, mag)
+                         : walk_chunk<T, P, W, false>(v, sU, sW, k0, nq, pc, mag);
     dd_acc(hi, lo, Num<T>::re(acc));
     if constexpr (sizeof(T) == 16) dd_acc(hi_i, lo_i, Num<T>::im(acc));
   }
