@@ -27,7 +27,7 @@ Scratch* scratch() {
   Scratch* s = &g_scratch[dev];
   if (s->device != dev) {
     s->device = dev;
-    if (cudaMallocHost(&s->host, 64 * sizeof(double)) != cudaSuccess) return nullptr;
+    if (cudaMallocHost(&s->host, kHostResultDoubles * sizeof(double)) != cudaSuccess) return nullptr;
   }
   return s;
 }
@@ -43,6 +43,23 @@ int ensure_dev(Scratch* s, size_t bytes) {
   size_t cap = std::max<size_t>(bytes, 1 << 20);
   PERM_CUDA_TRY(cudaMalloc(&s->dev, cap));
   s->dev_cap = cap;
+  return PERM_OK;
+}
+
+int stage_h2d(Scratch* s, void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+  if (s->stage_cap < bytes) {
+    if (s->stage) cudaFreeHost(s->stage);
+    s->stage = nullptr;
+    s->stage_cap = 0;
+    const size_t cap = std::max<size_t>(bytes, 1 << 16);
+    PERM_CUDA_TRY(cudaMallocHost(&s->stage, cap));
+    s->stage_cap = cap;
+  }
+  // the staging buffer (and the scratch it feeds) may still be in use by an
+  // asynchronous call queued earlier on this stream
+  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  std::memcpy(s->stage, src, bytes);
+  PERM_CUDA_TRY(cudaMemcpyAsync(dst, s->stage, bytes, cudaMemcpyHostToDevice, stream));
   return PERM_OK;
 }
 
@@ -302,18 +319,8 @@ int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, dou
   if (st) return st;
   double* partials = static_cast<double*>(s->dev);
   double* data = partials + (size_t)kMaxPartials * kPartialStride;
-  // stage through pinned memory so the H2D copy is a true async DMA; the
-  // previous call on this thread has synchronized, so the buffer is free
-  if (s->stage_cap < data_bytes) {
-    if (s->stage) cudaFreeHost(s->stage);
-    s->stage = nullptr;
-    s->stage_cap = 0;
-    PERM_CUDA_TRY(cudaMallocHost(&s->stage, std::max<size_t>(data_bytes, 1 << 16)));
-    s->stage_cap = std::max<size_t>(data_bytes, 1 << 16);
-  }
-  PERM_CUDA_TRY(cudaStreamSynchronize(stream));  // staging buffer may still feed an async call
-  std::memcpy(s->stage, ws.buf.data(), data_bytes);
-  PERM_CUDA_TRY(cudaMemcpyAsync(data, s->stage, data_bytes, cudaMemcpyHostToDevice, stream));
+  st = stage_h2d(s, data, ws.buf.data(), data_bytes, stream);
+  if (st) return st;
   walk_fn fn = walk_lookup(ws.cplx ? 1 : 0, ws.weighted, ws.P);
   if (!fn) {
     set_error("no walk kernel for this state length");

@@ -30,12 +30,15 @@ struct Scratch {
   int device = -1;
   void* dev = nullptr;       // device scratch
   size_t dev_cap = 0;
-  double* host = nullptr;    // pinned host result buffer (64 doubles)
+  double* host = nullptr;    // pinned host result buffer (kHostResultDoubles)
   void* stage = nullptr;     // pinned host staging buffer for H2D copies
   size_t stage_cap = 0;
   cudaStream_t own = nullptr;
 };
+constexpr size_t kHostResultDoubles = 16384;    // pinned result buffer size
 Scratch* scratch();                              // for the current device
+// copy host bytes to device through the pinned staging buffer (async DMA)
+int stage_h2d(Scratch* s, void* dst, const void* src, size_t bytes, cudaStream_t stream);
 int ensure_dev(Scratch* s, size_t bytes);        // grow device scratch
 cudaStream_t pick_stream(void* stream);
 

@@ -30,12 +30,20 @@ static const std::vector<uint64_t>& binom_table() {
   return t;
 }
 
-struct CombRun {
-  void* buf = nullptr;
-  ~CombRun() {
-    if (buf) cudaFree(buf);
+static int device_binom_table(const uint64_t** out) {
+  static uint64_t* tabs[16] = {nullptr};
+  int dev = 0;
+  PERM_CUDA_TRY(cudaGetDevice(&dev));
+  if (!tabs[dev & 15]) {
+    const auto& bt = binom_table();
+    uint64_t* d = nullptr;
+    PERM_CUDA_TRY(cudaMalloc(&d, bt.size() * 8));
+    PERM_CUDA_TRY(cudaMemcpy(d, bt.data(), bt.size() * 8, cudaMemcpyHostToDevice));
+    tabs[dev & 15] = d;
   }
-};
+  *out = tabs[dev & 15];
+  return PERM_OK;
+}
 
 static int target_threads() {
   int dev = 0, nsm = 148;
@@ -67,8 +75,11 @@ static int launch_comb(bool ryser, const void* dA, const uint64_t* dB, int m, in
   else comb_dfs_kernel<MODE><<<(unsigned)blocks, kCombThreads, 0, stream>>>(a);
   PERM_CUDA_TRY(cudaGetLastError());
   host->resize(blocks * 8);
-  PERM_CUDA_TRY(cudaMemcpyAsync(host->data(), dOut, blocks * 64, cudaMemcpyDeviceToHost, stream));
+  Scratch* sc = scratch();
+  if (blocks * 8 > kHostResultDoubles) return cuda_fail(cudaErrorInvalidValue, "comb partials exceed host buffer");
+  PERM_CUDA_TRY(cudaMemcpyAsync(sc->host, dOut, blocks * 64, cudaMemcpyDeviceToHost, stream));
   PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  std::memcpy(host->data(), sc->host, blocks * 64);
   return PERM_OK;
 }
 
@@ -132,14 +143,20 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
   const uint64_t thr = (uint64_t)target_threads();
   const size_t max_blocks = (thr + kCombThreads - 1) / kCombThreads + 1;
   const size_t bytes = hA.size() + bt.size() * 8 + max_blocks * 64 + 256;
-  CombRun run;
-  PERM_CUDA_TRY(cudaMallocAsync(&run.buf, bytes, stream));
-  unsigned char* base = static_cast<unsigned char*>(run.buf);
+  // engine-owned scratch (no per-call allocation): [matrix][block partials];
+  // the binomial table lives on the device once per device
+  Scratch* sc = scratch();
+  if (!sc) return cuda_fail(cudaErrorNoDevice, "scratch");
+  int st0 = ensure_dev(sc, bytes);
+  if (st0) return st0;
+  const uint64_t* dB = nullptr;
+  st0 = device_binom_table(&dB);
+  if (st0) return st0;
+  unsigned char* base = static_cast<unsigned char*>(sc->dev);
   void* dA = base;
-  uint64_t* dB = reinterpret_cast<uint64_t*>(base + ((hA.size() + 15) & ~(size_t)15));
-  void* dOut = dB + bt.size();
-  PERM_CUDA_TRY(cudaMemcpyAsync(dA, hA.data(), hA.size(), cudaMemcpyHostToDevice, stream));
-  PERM_CUDA_TRY(cudaMemcpyAsync(dB, bt.data(), bt.size() * 8, cudaMemcpyHostToDevice, stream));
+  void* dOut = base + ((hA.size() + 255) & ~(size_t)255);
+  st0 = stage_h2d(sc, dA, hA.data(), hA.size(), stream);
+  if (st0) return st0;
   std::vector<int64_t> h;
   int st = PERM_OK;
   if (ryser) {
@@ -205,8 +222,6 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
       if (mode == 1) out[1] = jh + jl;
     }
   }
-  PERM_CUDA_TRY(cudaFreeAsync(run.buf, stream));
-  run.buf = nullptr;
   PERM_CUDA_TRY(cudaStreamSynchronize(stream));
   return PERM_OK;
 }

@@ -149,9 +149,17 @@ __host__ __device__ constexpr int row_stride() { return (sizeof(T) == 8) ? ((P +
 // P/kChains, only kChains temporaries live (a full pairwise tree keeps P/2
 // extra values live and spills at P >= 20).
 #ifndef WALK_CHAINS
-#define WALK_CHAINS 8
+#define WALK_CHAINS 4
 #endif
 constexpr int kChains = WALK_CHAINS;
+#ifndef WALK_FUSED
+#define WALK_FUSED 1
+#endif
+#if WALK_FUSED
+#define WALK_CHUNK walk_chunk_fused
+#else
+#define WALK_CHUNK walk_chunk
+#endif
 template <typename T, int N>
 __device__ __forceinline__ T tree_of(const T (&c)[N]) {
   if constexpr (N == 1) {
@@ -200,6 +208,89 @@ struct Term {
     }
   }
 };
+
+// Fused step: the term of the current state (sign or popcount weight) and
+// the update to the next state, interleaved column by column -- column j
+// enters its product chain, then takes its row update -- so each U row pair
+// is loaded right where it is consumed and the products of step s overlap
+// the shared-memory latency of step s+1's row.  UPD: 0 add, 1 sub, 2 fma(s).
+template <typename T, int P, bool W, bool MAG, int UPD>
+__device__ __forceinline__ void term_update(T (&v)[P], const T* __restrict__ row, double s, int sign, int pc,
+                                            const double* sW, T& acc, double& mag) {
+  constexpr int C = (P < kChains) ? P : kChains;
+  T c[C];
+  auto upd = [&](T x, T u) -> T {
+    if constexpr (UPD == 0) return Num<T>::add(x, u);
+    else if constexpr (UPD == 1) return Num<T>::sub(x, u);
+    else return Num<T>::fmas(s, u, x);
+  };
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    T u;
+    if constexpr (sizeof(T) == 8) {
+      if ((j & 1) == 0 && j + 1 < P) {
+        const double2 u2 = lds2(row + j);
+        u = u2.x;
+        if (j < C) c[j] = v[j]; else c[j % C] = Num<T>::mul(c[j % C], v[j]);
+        v[j] = upd(v[j], u);
+        if (j + 1 < C) c[j + 1] = v[j + 1]; else c[(j + 1) % C] = Num<T>::mul(c[(j + 1) % C], v[j + 1]);
+        v[j + 1] = upd(v[j + 1], u2.y);
+        continue;
+      }
+      if (j & 1) continue;  // consumed with its pair
+      u = lds1(row + j);
+    } else {
+      u = ld_row<T>(row, j);
+    }
+    if (j < C) c[j] = v[j]; else c[j % C] = Num<T>::mul(c[j % C], v[j]);
+    v[j] = upd(v[j], u);
+  }
+  const T p = tree_of<T, C>(c);
+  if constexpr (W) {
+    const double wt = sW[pc];
+    acc = Num<T>::add(acc, Num<T>::scale(wt, p));
+    if constexpr (MAG) mag += fabs(wt) * Num<T>::absval(p);
+  } else {
+    acc = (sign > 0) ? Num<T>::add(acc, p) : Num<T>::sub(acc, p);
+    if constexpr (MAG) mag += Num<T>::absval(p);
+  }
+}
+
+template <typename T, int P, bool W, bool MAG>
+__device__ __forceinline__ T walk_chunk_fused(T (&v)[P], const T* sU, const double* sW, uint64_t k0, uint64_t nq,
+                                              int pc, double& mag) {
+  constexpr int PS = row_stride<T, P>();
+  T acc = Num<T>::zero();
+  for (uint64_t q = 0; q < nq; ++q) {
+    // T0+U1(+U0), T1+U2(+U1), T2+U3(-U0), T3+U4(+-U2), T4+U5(+U0), T5+U6(-U1), T6+U7(-U0)
+    term_update<T, P, W, MAG, 0>(v, sU, 0.0, +1, pc, sW, acc, mag);
+    if constexpr (W) ++pc;
+    term_update<T, P, W, MAG, 0>(v, sU + PS, 0.0, -1, pc, sW, acc, mag);
+    if constexpr (W) ++pc;
+    term_update<T, P, W, MAG, 1>(v, sU, 0.0, +1, pc, sW, acc, mag);
+    if constexpr (W) --pc;
+    const int b3 = (int)(((k0 + (q << 3)) >> 3) & 1);  // U4: bit 2 set iff bit 3 of k0+8q clear
+    term_update<T, P, W, MAG, 2>(v, sU + 2 * PS, b3 ? -1.0 : 1.0, -1, pc, sW, acc, mag);
+    if constexpr (W) pc += b3 ? -1 : 1;
+    term_update<T, P, W, MAG, 0>(v, sU, 0.0, +1, pc, sW, acc, mag);
+    if constexpr (W) ++pc;
+    term_update<T, P, W, MAG, 1>(v, sU + PS, 0.0, -1, pc, sW, acc, mag);
+    if constexpr (W) --pc;
+    term_update<T, P, W, MAG, 1>(v, sU, 0.0, +1, pc, sW, acc, mag);
+    if constexpr (W) --pc;
+    if (q + 1 < nq) {  // T7 + the runtime row update that opens the next 8 steps
+      const uint64_t l0 = (q + 1) << 3;
+      const int t = __ffsll((long long)l0) - 1;
+      const uint64_t k = k0 + l0;
+      const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
+      term_update<T, P, W, MAG, 2>(v, sU + t * PS, set ? 1.0 : -1.0, -1, pc, sW, acc, mag);
+      if constexpr (W) pc += set ? 1 : -1;
+    } else {
+      Term<T, P, W, MAG>::add(v, -1, pc, sW, acc, mag);
+    }
+  }
+  return acc;
+}
 
 // The 8-step unrolled walk over one chunk of nq*8 indices starting at k0
 // (state v already seeded): every flip row but one per 8 steps is a
@@ -314,8 +405,8 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_ke
       }
     }
     const int pc = __popcll(g0);
-    const T acc = mag_on ? walk_chunk<T, P, W, true>(v, sU, sW, k0, nq, pc, mag)
-                         : walk_chunk<T, P, W, false>(v, sU, sW, k0, nq, pc, mag);
+    const T acc = mag_on ? WALK_CHUNK<T, P, W, true>(v, sU, sW, k0, nq, pc, mag)
+                         : WALK_CHUNK<T, P, W, false>(v, sU, sW, k0, nq, pc, mag);
     dd_acc(hi, lo, Num<T>::re(acc));
     if constexpr (sizeof(T) == 16) dd_acc(hi_i, lo_i, Num<T>::im(acc));
   }
@@ -350,12 +441,12 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_ke
 
 // Single-thread walk for tiny index spaces (< 32 chunks of 8): runtime P.
 // Same arithmetic as walk_kernel (plain sum per 'chunk' of the whole range).
-template <typename T>
+template <typename T, int P>
 __global__ void walk_small_kernel(const T* __restrict__ v0, const T* __restrict__ U, const double* __restrict__ w,
-                                  int P, int B, int weighted, int mag_on, uint64_t k_begin, uint64_t k_end,
+                                  int /*P*/, int B, int weighted, int mag_on, uint64_t k_begin, uint64_t k_end,
                                   double* partials) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  T v[64];
+  T v[P];
   const uint64_t g0 = k_begin ^ (k_begin >> 1);
   for (int j = 0; j < P; ++j) v[j] = v0[j];
   for (int t = 0; t < B; ++t)

@@ -34,13 +34,25 @@ constexpr int kMaxPartials = 148 * 16;
 // Chunk length for a range of `steps` Gray indices over `lanes` threads:
 // long chunks amortize seeding (~6 row FMAs + B/64 sums per chunk), many
 // chunks per lane bound the tail of the static lane->chunk assignment.
+// Cost model: a warp processes ceil(groups / warps) groups of 32 chunks, each
+// chunk costing L steps plus ~3 steps' worth of seeding (6 row FMAs + the
+// warp-cooperative column sums); pick the L = 2^r (8 <= L <= 2^14) that
+// minimizes the slowest warp's work.
 inline int choose_log2L(uint64_t steps, uint64_t lanes) {
-  int r = 3;
-  // grow L while every lane still gets >= 24 chunks and L <= 2^14
-  while (r < 14 && (steps >> (r + 1)) >= 24 * lanes) ++r;
-  // need at least 32 chunks (one warp-group)
-  while (r > 3 && (steps >> r) < 32) --r;
-  return r;
+  const uint64_t warps = lanes / 32 ? lanes / 32 : 1;
+  int best = 3;
+  double best_cost = 1e300;
+  for (int r = 3; r <= 14; ++r) {
+    const uint64_t groups = (steps >> r) / 32;
+    if (groups < 1) break;
+    const uint64_t per_warp = (groups + warps - 1) / warps;
+    const double cost = (double)per_warp * ((double)(1ull << r) + 3.0);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = r;
+    }
+  }
+  return best;
 }
 
 // Largest power-of-two alignment that divides x (x != 0), capped.
@@ -74,7 +86,7 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
     plan->small = true;
     plan->grid = 1;
     plan->log2L = 0;
-    walk_small_kernel<T><<<1, 32, 0, stream>>>(static_cast<const T*>(job.v0), static_cast<const T*>(job.U), job.w,
+    walk_small_kernel<T, P><<<1, 32, 0, stream>>>(static_cast<const T*>(job.v0), static_cast<const T*>(job.U), job.w,
                                                P, job.B, W ? 1 : 0, job.mag, job.k_begin, job.k_end, job.partials);
     return cudaGetLastError();
   }

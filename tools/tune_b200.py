@@ -1,0 +1,83 @@
+"""B200 dispatch retune (north_star item 5), the reference tuner's procedure
+(src/tuner.py:286-310) on GPU timings.
+
+    python tools/tune_b200.py collect gpurun_out/tune_timings.json   # on the GPU box
+    python tools/tune_b200.py fit gpurun_out/tune_timings.json        # here: fit + emit
+
+collect: for every grid shape (n = 2..24, r in {1/8, ..., 1}, m = max(1,
+round(r n)), as src/tuner.py:27-28) time combinatoric / Ryser / Glynn through
+the public mid-level API (run_algorithm on a host float64 matrix: staging,
+kernels, result read-back), median of `trials` calls after a warm-up.
+Combinatoric is skipped above 5e7 permutations (src/tuner.py:33-34 caps it
+similarly).  fit: p1..p8 by tuning.fit_params, written to
+paper_2510_03421_b200/tuned/b200.tuning (format v1).
+"""
+from __future__ import annotations
+
+import json
+import math
+import statistics
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+RATIOS = (1 / 8, 1 / 4, 3 / 8, 1 / 2, 5 / 8, 3 / 4, 7 / 8, 1.0)
+
+
+def collect(out_path, trials=7):
+    from paper_2510_03421_b200.algorithms import AlgorithmId, run_algorithm
+    from paper_2510_03421_b200.core import as_matrix
+
+    rng = np.random.default_rng(0)
+    res = {}
+    shapes = sorted({(max(1, round(r * n)), n) for n in range(2, 25) for r in RATIOS})
+    for m, n in shapes:
+        a = as_matrix(rng.uniform(-1, 1, (m, n)))
+        cell = {}
+        for alg in AlgorithmId:
+            if alg is AlgorithmId.COMBINATORIC and math.perm(n, m) > 5e7:
+                continue
+            run_algorithm(a, alg)  # warm-up (module load, allocation)
+            ts = []
+            for _ in range(trials):
+                t = time.perf_counter()
+                run_algorithm(a, alg)
+                ts.append(time.perf_counter() - t)
+            cell[alg.value] = statistics.median(ts)
+        res[f"{m},{n}"] = cell
+        print(m, n, {k: f"{v * 1e6:.0f}us" for k, v in cell.items()}, flush=True)
+    Path(out_path).write_text(json.dumps(res, indent=1))
+
+
+def fit(in_path):
+    from paper_2510_03421_b200.tuning import emit_tuning_file, fit_params
+
+    raw = json.loads(Path(in_path).read_text())
+    timings = {tuple(int(x) for x in k.split(",")): v for k, v in raw.items()}
+    p = fit_params(timings, host="NVIDIA B200 (sm_100a)")
+    out = ROOT / "paper_2510_03421_b200" / "tuned" / "b200.tuning"
+    out.parent.mkdir(exist_ok=True)
+    emit_tuning_file(p, out)
+    print(out.read_text())
+    # report the dispatch slowdown over the grid
+    from paper_2510_03421_b200.dispatch import default_params, select_algorithm
+
+    for name, params in (("b200", p), ("default", default_params())):
+        slow = []
+        for (m, n), t in timings.items():
+            pick = select_algorithm(m, n, params).value
+            slow.append(t[pick] / min(t.values()) if pick in t else float("inf"))
+        print(f"{name}: mean slowdown {statistics.mean(slow):.3f} max {max(slow):.2f} "
+              f"cells within 1.25x: {sum(s <= 1.25 for s in slow)}/{len(slow)}")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "collect":
+        collect(sys.argv[2])
+    else:
+        fit(sys.argv[2])
