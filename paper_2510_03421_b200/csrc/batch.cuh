@@ -19,6 +19,7 @@
 //     runtime loops, for shapes without a template.
 #pragma once
 #include "common.cuh"
+#include "walk.cuh"
 
 namespace permb200 {
 
@@ -159,6 +160,58 @@ __global__ void __launch_bounds__(kBatchThreads) batch_glynn_kernel(const T* __r
   }
 }
 
+// -------------------------------------------------------- Glynn, warp/matrix
+// For batches too small to fill the device with one thread per matrix (C1:
+// 64 x 12x12), a warp walks one matrix: lane l owns the Gray chunk
+// [l*L, (l+1)*L), L = 2^(N-1)/32, and runs the same fused 8-step walk as
+// walk_kernel on the matrix's -2*rows staged in shared memory (warp-uniform
+// reads: broadcasts).  Needs N >= 9 (L >= 8).
+constexpr int kBatchWarpMats = 8;  // matrices (warps) per block
+
+template <typename T, int N>
+__global__ void __launch_bounds__(32 * kBatchWarpMats) batch_glynn_warp_kernel(const T* __restrict__ a,
+                                                                              T* __restrict__ out, int64_t nbatch) {
+  constexpr int PS = row_stride<T, N>();
+  constexpr int SLOT = (N - 1) * PS + PS;  // U rows + column sums
+  __shared__ __align__(16) T smem[kBatchWarpMats * SLOT];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t mat = (int64_t)blockIdx.x * kBatchWarpMats + warp;
+  if (mat >= nbatch) return;  // whole warp exits together
+  T* sU = smem + warp * SLOT;
+  T* sV0 = sU + (N - 1) * PS;
+  const T* A = a + mat * N * N;
+  for (int e = lane; e < N * N; e += 32) {
+    const int i = e / N, j = e - i * N;
+    if (i >= 1) sU[(N - 1 - i) * PS + j] = Num<T>::scale(-2.0, A[e]);  // U[t] = -2 row(N-1-t)
+  }
+  for (int j = lane; j < N; j += 32) {
+    T s = A[j];
+    for (int i = 1; i < N; ++i) s = Num<T>::add(s, A[i * N + j]);
+    sV0[j] = s;
+  }
+  __syncwarp();
+  constexpr int LOG2L = N - 1 - 5;
+  const uint64_t k0 = (uint64_t)lane << LOG2L;
+  const uint64_t g0 = k0 ^ (k0 >> 1);
+  T v[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) v[j] = sV0[j];
+  for (int t = LOG2L - 1; t < N - 1; ++t)
+    if ((g0 >> t) & 1) row_add<T, N>(v, sU + t * PS);
+  double mag = 0.0;
+  T acc = walk_chunk_fused<T, N, false, false>(v, sU, nullptr, k0, 1ull << (LOG2L - 3), 0, mag);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    if constexpr (sizeof(T) == 8) {
+      acc = acc + __shfl_down_sync(0xffffffffu, acc, off);
+    } else {
+      acc.x += __shfl_down_sync(0xffffffffu, acc.x, off);
+      acc.y += __shfl_down_sync(0xffffffffu, acc.y, off);
+    }
+  }
+  if (lane == 0) out[mat] = Num<T>::scale(1.0 / (double)(1 << (N - 1)), acc);
+}
+
 // ---------------------------------------------------------------- Ryser
 template <typename T, int M, int N>
 __device__ T batch_ryser_one(const T* __restrict__ A /* smem, row stride N */, const double* __restrict__ w) {
@@ -167,15 +220,61 @@ __device__ T batch_ryser_one(const T* __restrict__ A /* smem, row stride N */, c
   for (int i = 0; i < M; ++i) v[i] = Num<T>::zero();
   T acc = Num<T>::zero();
   int pc = 0;
-  for (int k = 1; k < (1 << N); ++k) {
-    const int t = __ffs(k) - 1;
-    const bool set = ((k ^ (k >> 1)) >> t) & 1;
+  if constexpr (N < 3) {
+    for (int k = 1; k < (1 << N); ++k) {
+      const int t = __ffs(k) - 1;
+      const bool set = ((k ^ (k >> 1)) >> t) & 1;
 #pragma unroll
-    for (int i = 0; i < M; ++i) v[i] = set ? Num<T>::add(v[i], A[i * N + t]) : Num<T>::sub(v[i], A[i * N + t]);
-    pc += set ? 1 : -1;
-    if (pc <= M) acc = Num<T>::add(acc, Num<T>::scale(w[pc], prod_chain<T, M>(v)));
+      for (int i = 0; i < M; ++i) v[i] = set ? Num<T>::add(v[i], A[i * N + t]) : Num<T>::sub(v[i], A[i * N + t]);
+      pc += set ? 1 : -1;
+      if (pc <= M) acc = Num<T>::add(acc, Num<T>::scale(w[pc], prod_chain<T, M>(v)));
+    }
+    return acc;
+  } else {
+    // columns 0, 1, 2 (7 of every 8 flips) in registers; Gray schedule
+    // unrolled by 8 as in batch_glynn_one; subsets larger than M skipped
+    // (their weight is 0) -- pc is the same for every thread: uniform branch
+    T c0[M], c1[M], c2[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      c0[i] = A[i * N + 0];
+      c1[i] = A[i * N + 1];
+      c2[i] = A[i * N + 2];
+    }
+#define RB_TERM()                                                                   \
+  if (pc <= M) acc = Num<T>::add(acc, Num<T>::scale(w[pc], prod_chain<T, M>(v)));
+#define RB_STEP(C, OP, D)                                                           \
+  _Pragma("unroll") for (int i = 0; i < M; ++i) v[i] = Num<T>::OP(v[i], C[i]);    \
+  pc += D;                                                                          \
+  RB_TERM()
+    constexpr int NQ = (1 << N) / 8;
+    for (int q = 0; q < NQ; ++q) {
+      if (q) {
+        const int l0 = q << 3;
+        const int t = __ffs(l0) - 1;  // >= 3
+        const bool set = ((l0 ^ (l0 >> 1)) >> t) & 1;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+          v[i] = set ? Num<T>::add(v[i], A[i * N + t]) : Num<T>::sub(v[i], A[i * N + t]);
+        pc += set ? 1 : -1;
+        RB_TERM()
+      }
+      RB_STEP(c0, add, 1)   // l = 1
+      RB_STEP(c1, add, 1)   // l = 2
+      RB_STEP(c0, sub, -1)  // l = 3
+      if ((q & 1) == 0) {   // l = 4
+        RB_STEP(c2, add, 1)
+      } else {
+        RB_STEP(c2, sub, -1)
+      }
+      RB_STEP(c0, add, 1)   // l = 5
+      RB_STEP(c1, sub, -1)  // l = 6
+      RB_STEP(c0, sub, -1)  // l = 7
+    }
+#undef RB_STEP
+#undef RB_TERM
+    return acc;
   }
-  return acc;
 }
 
 template <typename T, int M, int N>

@@ -28,6 +28,14 @@ Scratch* scratch() {
   if (s->device != dev) {
     s->device = dev;
     if (cudaMallocHost(&s->host, kHostResultDoubles * sizeof(double)) != cudaSuccess) return nullptr;
+    // keep stream-ordered allocations cached across synchronizations (the
+    // default release threshold of 0 returns them to the driver at every
+    // sync, which made each batch call pay ~2 ms of re-mapping)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
   }
   return s;
 }
@@ -64,6 +72,7 @@ int stage_h2d(Scratch* s, void* dst, const void* src, size_t bytes, cudaStream_t
 }
 
 cudaStream_t pick_stream(void* stream) {
+  (void)scratch();  // per-device setup (pinned buffers, mem-pool threshold) on first use
   return stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
 }
 

@@ -1,5 +1,9 @@
 // Host side of the batched small-matrix kernels (perm_batch_*).
+#include <algorithm>
+#include <cstring>
+#include <thread>
 #include <utility>
+#include <vector>
 
 #include "batch.cuh"
 #include "engine.cuh"
@@ -83,6 +87,105 @@ static cudaError_t launch_generic(const void* a, void* out, int64_t B, int m, in
   return cudaGetLastError();
 }
 
+template <typename T, int N>
+static cudaError_t launch_bglynn_warp(const void* a, void* out, int64_t B, cudaStream_t s) {
+  const int64_t grid = (B + kBatchWarpMats - 1) / kBatchWarpMats;
+  batch_glynn_warp_kernel<T, N><<<(unsigned)grid, 32 * kBatchWarpMats, 0, s>>>(static_cast<const T*>(a),
+                                                                               static_cast<T*>(out), B);
+  return cudaGetLastError();
+}
+template <typename T, int... Ns>
+static batch_fn pick_glynn_warp(int n, std::integer_sequence<int, Ns...>) {
+  batch_fn f = nullptr;
+  ((n == Ns + 9 ? (f = &launch_bglynn_warp<T, Ns + 9>, 0) : 0), ...);
+  return f;
+}
+
+// Kernel choice for one (device-resident) batch.  Thread-per-matrix needs
+// enough matrices to fill the GPU; below that a warp per matrix (n >= 9).
+static int launch_batch(int alg, bool cplx, int64_t B, int m, int n, const void* dA, void* dOut,
+                        cudaStream_t stream) {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  batch_fn fn = nullptr;
+  if (alg == PERM_ALG_GLYNN && m == n && n >= 9 && n <= 16 && B < (int64_t)nsm * 512)
+    fn = cplx ? pick_glynn_warp<cd>(n, std::make_integer_sequence<int, 8>{})
+              : pick_glynn_warp<double>(n, std::make_integer_sequence<int, 8>{});
+  if (!fn && alg == PERM_ALG_GLYNN && m == n && n >= 2 && n <= 12)
+    fn = cplx ? pick_glynn<cd>(n, std::make_integer_sequence<int, 11>{})
+              : pick_glynn<double>(n, std::make_integer_sequence<int, 11>{});
+  if (!fn && alg == PERM_ALG_RYSER && m < n && n <= 12)
+    fn = cplx ? pick_ryser<cd>(m, n, std::make_integer_sequence<int, 66>{})
+              : pick_ryser<double>(m, n, std::make_integer_sequence<int, 66>{});
+  cudaError_t e;
+  if (fn) e = fn(dA, dOut, B, stream);
+  else e = cplx ? launch_generic<cd>(dA, dOut, B, m, n, alg, stream)
+                : launch_generic<double>(dA, dOut, B, m, n, alg, stream);
+  return e == cudaSuccess ? PERM_OK : cuda_fail(e, "batch kernel launch");
+}
+
+// Two-slot pinned staging for host batches (per host thread, per device).
+struct BatchPipe {
+  int device = -1;
+  void *hin[2] = {nullptr, nullptr}, *hout[2] = {nullptr, nullptr};
+  void *din[2] = {nullptr, nullptr}, *dout[2] = {nullptr, nullptr};
+  size_t in_cap = 0, out_cap = 0;
+  cudaStream_t stream[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  int64_t pending[2] = {0, 0}, pending_first[2] = {0, 0};
+  int ensure(size_t in_b, size_t out_b) {
+    if (!stream[0]) {
+      for (int i = 0; i < 2; ++i) {
+        PERM_CUDA_TRY(cudaStreamCreateWithFlags(&stream[i], cudaStreamNonBlocking));
+        PERM_CUDA_TRY(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+        PERM_CUDA_TRY(cudaEventRecord(done[i], stream[i]));
+      }
+    }
+    if (in_b > in_cap || out_b > out_cap) {
+      for (int i = 0; i < 2; ++i) {
+        PERM_CUDA_TRY(cudaEventSynchronize(done[i]));
+        if (hin[i]) cudaFreeHost(hin[i]);
+        if (hout[i]) cudaFreeHost(hout[i]);
+        if (din[i]) cudaFree(din[i]);
+        if (dout[i]) cudaFree(dout[i]);
+        PERM_CUDA_TRY(cudaMallocHost(&hin[i], in_b));
+        PERM_CUDA_TRY(cudaMallocHost(&hout[i], out_b));
+        PERM_CUDA_TRY(cudaMalloc(&din[i], in_b));
+        PERM_CUDA_TRY(cudaMalloc(&dout[i], out_b));
+      }
+      in_cap = in_b;
+      out_cap = out_b;
+    }
+    return PERM_OK;
+  }
+};
+static thread_local BatchPipe g_pipe[16];
+static BatchPipe& batch_pipe() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return g_pipe[dev & 15];
+}
+
+// Host memcpy split over a few threads (pageable -> pinned staging).
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t kMin = 8u << 20;
+  if (bytes < kMin) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const int nt = 4;
+  std::vector<std::thread> th;
+  const size_t part = (bytes + nt - 1) / nt;
+  for (int i = 0; i < nt; ++i) {
+    const size_t off = (size_t)i * part;
+    if (off >= bytes) break;
+    const size_t len = std::min(part, bytes - off);
+    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len); });
+  }
+  for (auto& t : th) t.join();
+}
+
 int batch_select(int m, int n) {
   // thread-per-matrix fast paths: Glynn for squares, subset-skipping Ryser
   // for rectangles (cheapest exact per-matrix work for C2a / C2b)
@@ -113,35 +216,47 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
   if (B == 0) return PERM_OK;
   cudaStream_t stream = pick_stream(stream_);
   const size_t esz = cplx ? 16 : 8;
-  const size_t in_bytes = (size_t)B * m * n * esz, out_bytes = (size_t)B * esz;
-  const void* dA = a;
-  void* dOut = out;
-  void* buf = nullptr;
-  if (!dev_ptr) {
-    PERM_CUDA_TRY(cudaMallocAsync(&buf, in_bytes + out_bytes + 256, stream));
-    dA = buf;
-    dOut = static_cast<char*>(buf) + ((in_bytes + 255) & ~(size_t)255);
-    PERM_CUDA_TRY(cudaMemcpyAsync(const_cast<void*>(dA), a, in_bytes, cudaMemcpyHostToDevice, stream));
+  const size_t mat_bytes = (size_t)m * n * esz;
+  if (dev_ptr) return launch_batch(alg, cplx, B, m, n, a, out, stream);
+  // Host arrays: chunked pipeline through two pinned staging slots on two
+  // engine streams, so the host copy of chunk c+1, the H2D DMA of chunk c and
+  // the kernels overlap (the input is read from pageable numpy memory).
+  Scratch* sc = scratch();
+  if (!sc) return cuda_fail(cudaErrorNoDevice, "scratch");
+  int64_t chunk = std::max<int64_t>(1, (int64_t)((32u << 20) / mat_bytes));
+  chunk = std::min<int64_t>(chunk, B);
+  const size_t in_chunk = (size_t)chunk * mat_bytes, out_chunk = (size_t)chunk * esz;
+  BatchPipe& bp = batch_pipe();
+  int st = bp.ensure(in_chunk, out_chunk);
+  if (st) return st;
+  for (int64_t c0 = 0, it = 0; c0 < B; c0 += chunk, ++it) {
+    const int slot = (int)(it & 1);
+    const int64_t cnt = std::min<int64_t>(chunk, B - c0);
+    // slot reuse: wait for its previous chunk, then hand its results back
+    PERM_CUDA_TRY(cudaEventSynchronize(bp.done[slot]));
+    if (bp.pending[slot] > 0) {
+      std::memcpy(reinterpret_cast<char*>(out) + (size_t)bp.pending_first[slot] * esz, bp.hout[slot],
+                  (size_t)bp.pending[slot] * esz);
+      bp.pending[slot] = 0;
+    }
+    par_memcpy(bp.hin[slot], reinterpret_cast<const char*>(a) + (size_t)c0 * mat_bytes, (size_t)cnt * mat_bytes);
+    PERM_CUDA_TRY(cudaMemcpyAsync(bp.din[slot], bp.hin[slot], (size_t)cnt * mat_bytes, cudaMemcpyHostToDevice,
+                                  bp.stream[slot]));
+    st = launch_batch(alg, cplx, cnt, m, n, bp.din[slot], bp.dout[slot], bp.stream[slot]);
+    if (st) return st;
+    PERM_CUDA_TRY(cudaMemcpyAsync(bp.hout[slot], bp.dout[slot], (size_t)cnt * esz, cudaMemcpyDeviceToHost,
+                                  bp.stream[slot]));
+    PERM_CUDA_TRY(cudaEventRecord(bp.done[slot], bp.stream[slot]));
+    bp.pending[slot] = cnt;
+    bp.pending_first[slot] = c0;
   }
-  batch_fn fn = nullptr;
-  if (alg == PERM_ALG_GLYNN && m == n && n >= 2 && n <= 12)
-    fn = cplx ? pick_glynn<cd>(n, std::make_integer_sequence<int, 11>{})
-              : pick_glynn<double>(n, std::make_integer_sequence<int, 11>{});
-  if (alg == PERM_ALG_RYSER && m < n && n <= 12)
-    fn = cplx ? pick_ryser<cd>(m, n, std::make_integer_sequence<int, 66>{})
-              : pick_ryser<double>(m, n, std::make_integer_sequence<int, 66>{});
-  cudaError_t e;
-  if (fn) e = fn(dA, dOut, B, stream);
-  else e = cplx ? launch_generic<cd>(dA, dOut, B, m, n, alg, stream)
-                : launch_generic<double>(dA, dOut, B, m, n, alg, stream);
-  if (e != cudaSuccess) {
-    if (buf) cudaFreeAsync(buf, stream);
-    return cuda_fail(e, "batch kernel launch");
-  }
-  if (!dev_ptr) {
-    PERM_CUDA_TRY(cudaMemcpyAsync(out, dOut, out_bytes, cudaMemcpyDeviceToHost, stream));
-    PERM_CUDA_TRY(cudaFreeAsync(buf, stream));
-    PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  for (int slot = 0; slot < 2; ++slot) {
+    PERM_CUDA_TRY(cudaEventSynchronize(bp.done[slot]));
+    if (bp.pending[slot] > 0) {
+      std::memcpy(reinterpret_cast<char*>(out) + (size_t)bp.pending_first[slot] * esz, bp.hout[slot],
+                  (size_t)bp.pending[slot] * esz);
+      bp.pending[slot] = 0;
+    }
   }
   return PERM_OK;
 }

@@ -318,3 +318,20 @@ def test_batch_complex_and_device(rng):
     T = rng.uniform(-1, 1, (10, 5, 3))
     assert np.allclose(P.opt_batch(T), P.opt_batch(np.swapaxes(T, 1, 2)))
     assert P.opt_batch(np.zeros((0, 4, 4))).shape == (0,)
+
+
+def test_c1_batch_warp_per_matrix():
+    """64 x 12x12 (C1) through the batch API: small batches of n >= 9 run one
+    warp per matrix; results must match the reference like the per-matrix
+    path, real and complex, n = 9..16."""
+    d = np.load(GOLDEN / "c1.npz")
+    out = P.glynn_batch(d["a"])
+    for v, g in zip(out, d["glynn"]):
+        assert rel_err(v, g) <= TOL
+    rng = np.random.default_rng(11)
+    for n in (9, 13, 16):
+        A = rng.uniform(-1, 1, (40, n, n)) + 1j * rng.uniform(-1, 1, (40, n, n))
+        out = P.glynn_batch(A)
+        for i in (0, 17, 39):
+            v, M = P.permanent_with_magsum(as_matrix(A[i]), AlgorithmId.GLYNN)
+            assert scaled_err(out[i], v, M) <= TOL
