@@ -138,6 +138,15 @@ int perm_walk_finish_f64(int alg, int m, int n, const double* a, int64_t lda, co
 int perm_walk_finish_c128(int alg, int m, int n, const double* a, int64_t lda, const double* partials, int G,
                           double* out, double* magsum);
 
+/* ---- double-double validation walks -------------
+ * Glynn or Ryser with double-double state, products and sums (~1e-30 unit
+ * roundoff): the GPU cross-check where the reference cannot run and FP64
+ * Ryser is ill-conditioned.  out4 = {re_hi, re_lo, im_hi, im_lo} of the
+ * normalized permanent.  Synchronous; several times slower than the FP64
+ * walk (not a benchmark path). */
+int perm_permanent_dd(int alg, int cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out4,
+                      void* stream);
+
 /* ---- dispatch (src/dispatch.py:84-95) -----------------------------------
  * The reference's selection rule over (m, n) with parameters p[0..7] =
  * p1..p8; returns PERM_ALG_*.  batch/ngpu are reserved (0). */

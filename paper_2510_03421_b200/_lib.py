@@ -48,6 +48,7 @@ SIGNATURES = {
     "perm_batch_f64": (C.c_int, [C.c_int, C.c_int64, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp]),
     "perm_batch_c128": (C.c_int, [C.c_int, C.c_int64, C.c_int, C.c_int, _vp, _vp, C.c_int, _vp]),
     "perm_batch_select": (C.c_int, [C.c_int, C.c_int]),
+    "perm_permanent_dd": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _vp]),
     "perm_walk_steps": (C.c_uint64, [C.c_int, C.c_int, C.c_int]),
     "perm_walk_shard": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),

@@ -15,6 +15,8 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
 int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a, double* out, int dev_ptr,
                     void* stream);
 int batch_select(int m, int n);
+int dd_permanent(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out4,
+                 void* stream);
 }
 
 namespace {
@@ -254,6 +256,11 @@ int perm_batch_c128(int alg, int64_t B, int m, int n, const double* a, double* o
   return batch_permanent(alg, true, B, m, n, a, out, dev_ptr, stream);
 }
 int perm_batch_select(int m, int n) { return batch_select(m, n); }
+
+int perm_permanent_dd(int alg, int cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out4,
+                      void* stream) {
+  return dd_permanent(alg, cplx != 0, m, n, a, lda, dev_ptr, out4, stream);
+}
 
 uint64_t perm_walk_steps(int alg, int m, int n) {
   if (check_shape(alg, m, n)) return 0;

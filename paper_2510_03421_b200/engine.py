@@ -100,6 +100,19 @@ def exact_int(alg: str, a: np.ndarray, width: int = 64):
     return v, (not fits.value)
 
 
+def walk_dd(alg: str, a):
+    """Double-double Glynn / Ryser on the GPU (validation): returns
+    ((re_hi, re_lo), (im_hi, im_lo)) of the normalized permanent."""
+    lib = _lib.load()
+    cplx = np.iscomplexobj(a)
+    a = np.ascontiguousarray(a, dtype=np.complex128 if cplx else np.float64)
+    m, n = a.shape
+    out = _lib.out_buf(4)
+    st = lib.perm_permanent_dd(ALG_CODE[alg], int(cplx), m, n, C.c_void_p(a.ctypes.data), n, 0, out, None)
+    _lib.check(st, f"dd {alg} {m}x{n}")
+    return (out[0], out[1]), (out[2], out[3])
+
+
 def walk_steps(alg: str, m: int, n: int) -> int:
     return int(_lib.load().perm_walk_steps(ALG_CODE[alg], m, n))
 

@@ -335,3 +335,39 @@ def test_c1_batch_warp_per_matrix():
         for i in (0, 17, 39):
             v, M = P.permanent_with_magsum(as_matrix(A[i]), AlgorithmId.GLYNN)
             assert scaled_err(out[i], v, M) <= TOL
+
+
+def _dd_value(a, alg):
+    from paper_2510_03421_b200 import engine as E
+
+    (rh, rl), (ih, il) = E.walk_dd(alg, a)
+    return complex(rh + rl, ih + il) if np.iscomplexobj(a) else rh + rl
+
+
+@pytest.mark.parametrize("n", [14, 20])
+def test_gpu_double_double_walks_vs_oracle(n):
+    """The GPU double-double walks agree with the CPU double-double oracle."""
+    a = W.c5(n)
+    ref = O.dd_permanent("glynn", a)
+    for alg in ("glynn", "ryser"):
+        assert rel_err(_dd_value(a, alg), ref) <= 1e-13
+    c = W.c3a()[:n, :n]
+    ref = O.dd_permanent("glynn", c)
+    assert rel_err(_dd_value(c, "glynn"), ref) <= 1e-13
+    b = W.c3b()[: n - 4, :n]
+    ref = O.dd_permanent("ryser", b)
+    for alg in ("glynn", "ryser"):
+        assert rel_err(_dd_value(b, alg), ref) <= 1e-12
+
+
+def test_c5_glynn_vs_dd_ryser_n36():
+    """North-star C5 validation at full size: FP64 Glynn (the benchmarked
+    kernel) vs Ryser in double-double on the GPU (FP64 Ryser is useless here,
+    M_R/|per| ~ 1e18), and vs Glynn in double-double."""
+    a = W.c5(36)
+    v, M = P.permanent_with_magsum(as_matrix(a), AlgorithmId.GLYNN)
+    r = _dd_value(a, "ryser")
+    g = _dd_value(a, "glynn")
+    assert rel_err(g, r) <= 1e-12          # the two dd walks agree
+    assert scaled_err(v, r, M) <= TOL      # metric (ii) vs dd Ryser
+    assert rel_err(v, r) <= 1e-9           # plain relative error, reported
