@@ -61,6 +61,10 @@ int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, 
   if (st) return st;
   if (alg == PERM_ALG_RYSER && magsum == nullptr && ryser_rect_use_comb(m, n))
     return comb_permanent(true, cplx ? 1 : 0, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream_);
+  // walks shorter than one warp-group of chunks (Glynn n <= 8, Ryser n <= 7):
+  // the register-resident thread-per-matrix batch kernels, batch of one
+  if (magsum == nullptr && !dev_ptr && lda == n && walk_steps(alg, m, n) < 256)
+    return batch_permanent(alg, cplx, 1, m, n, a, out, 0, stream_);
   cudaStream_t stream = pick_stream(stream_);
   HostMat A;
   st = load_matrix(m, n, a, lda, dev_ptr, cplx, &A, stream);

@@ -52,10 +52,11 @@ static int target_threads() {
   return nsm * 4 * kCombThreads;
 }
 
-// Launch one ryser_comb / comb_dfs kernel and return per-block partials.
+// Enqueue one ryser_comb / comb_dfs kernel writing its per-block partials
+// (8 slots each) at dOut; returns the number of blocks.
 template <int MODE>
-static int launch_comb(bool ryser, const void* dA, const uint64_t* dB, int m, int n, int s, int depth,
-                       uint64_t total, void* dOut, std::vector<int64_t>* host, cudaStream_t stream) {
+static int enqueue_comb(bool ryser, const void* dA, const uint64_t* dB, int m, int n, int s, int depth,
+                        uint64_t total, void* dOut, uint64_t* nblocks, cudaStream_t stream) {
   const uint64_t thr = (uint64_t)target_threads();
   uint64_t per = (total + thr - 1) / thr;
   if (per < 1) per = 1;
@@ -74,12 +75,22 @@ static int launch_comb(bool ryser, const void* dA, const uint64_t* dB, int m, in
   if (ryser) ryser_comb_kernel<MODE><<<(unsigned)blocks, kCombThreads, 0, stream>>>(a);
   else comb_dfs_kernel<MODE><<<(unsigned)blocks, kCombThreads, 0, stream>>>(a);
   PERM_CUDA_TRY(cudaGetLastError());
-  host->resize(blocks * 8);
+  *nblocks = blocks;
+  return PERM_OK;
+}
+
+// One D2H of `count` 8-slot partials, then a single synchronization.
+static int fetch_partials(const void* dOut, uint64_t count, std::vector<int64_t>* host, cudaStream_t stream) {
+  host->resize(count * 8);
   Scratch* sc = scratch();
-  if (blocks * 8 > kHostResultDoubles) return cuda_fail(cudaErrorInvalidValue, "comb partials exceed host buffer");
-  PERM_CUDA_TRY(cudaMemcpyAsync(sc->host, dOut, blocks * 64, cudaMemcpyDeviceToHost, stream));
-  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
-  std::memcpy(host->data(), sc->host, blocks * 64);
+  if (count * 8 <= kHostResultDoubles) {
+    PERM_CUDA_TRY(cudaMemcpyAsync(sc->host, dOut, count * 64, cudaMemcpyDeviceToHost, stream));
+    PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+    std::memcpy(host->data(), sc->host, count * 64);
+  } else {
+    PERM_CUDA_TRY(cudaMemcpyAsync(host->data(), dOut, count * 64, cudaMemcpyDeviceToHost, stream));
+    PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  }
   return PERM_OK;
 }
 
@@ -141,7 +152,7 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
   const auto& bt = binom_table();
   // device buffers: matrix, binomials, partials
   const uint64_t thr = (uint64_t)target_threads();
-  const size_t max_blocks = (thr + kCombThreads - 1) / kCombThreads + 1;
+  const size_t max_blocks = ((thr + kCombThreads - 1) / kCombThreads + 1) * (size_t)(ryser ? m : 1);
   const size_t bytes = hA.size() + bt.size() * 8 + max_blocks * 64 + 256;
   // engine-owned scratch (no per-call allocation): [matrix][block partials];
   // the binomial table lives on the device once per device
@@ -164,22 +175,33 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
     double th = 0, tl = 0, ih = 0, il = 0;
     int64_t itotal = 0;
     bool ovf = false;
-    for (int s = m; s >= 1 && !ovf; --s) {
+    // all subset sizes enqueued back to back, one read-back
+    std::vector<uint64_t> first(m + 2, 0), cnt(m + 2, 0);
+    uint64_t off = 0;
+    for (int s = m; s >= 1; --s) {
       const uint64_t total = bt[n * 63 + s];
+      void* dst = static_cast<int64_t*>(dOut) + off * 8;
+      st = (mode == 2) ? enqueue_comb<kCombI64>(true, dA, dB, m, n, s, 0, total, dst, &cnt[s], stream)
+           : (mode == 0) ? enqueue_comb<kCombF64>(true, dA, dB, m, n, s, 0, total, dst, &cnt[s], stream)
+                         : enqueue_comb<kCombC128>(true, dA, dB, m, n, s, 0, total, dst, &cnt[s], stream);
+      if (st) return st;
+      first[s] = off;
+      off += cnt[s];
+    }
+    std::vector<int64_t> all;
+    st = fetch_partials(dOut, off, &all, stream);
+    if (st) return st;
+    for (int s = m; s >= 1 && !ovf; --s) {
       int64_t c = (int64_t)bt[(n - s) * 63 + (m - s)];
       const int64_t w = ((m - s) & 1) ? -c : c;
+      h.assign(all.begin() + first[s] * 8, all.begin() + (first[s] + cnt[s]) * 8);
       if (mode == 2) {
-        st = launch_comb<kCombI64>(true, dA, dB, m, n, s, 0, total, dOut, &h, stream);
-        if (st) return st;
         s128 size_sum;
         if (!combine_checked(h, &size_sum)) { ovf = true; break; }
         int64_t ss = (int64_t)size_sum, p;
         if (__builtin_mul_overflow(w, ss, &p) || __builtin_add_overflow(itotal, p, &itotal)) ovf = true;
       } else {
         double rh = 0, rl = 0, jh = 0, jl = 0;
-        st = (mode == 0) ? launch_comb<kCombF64>(true, dA, dB, m, n, s, 0, total, dOut, &h, stream)
-                         : launch_comb<kCombC128>(true, dA, dB, m, n, s, 0, total, dOut, &h, stream);
-        if (st) return st;
         combine_float(h, &rh, &rl, &jh, &jl);
         const double wd = (double)w;
         // w * size_sum in double-double (w exact up to 2^53)
@@ -204,7 +226,10 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
     if (D < 1) D = 1;
     const uint64_t total = nperm(n, D);
     if (mode == 2) {
-      st = launch_comb<kCombI64>(false, dA, dB, m, n, 0, D, total, dOut, &h, stream);
+      uint64_t nb = 0;
+      st = enqueue_comb<kCombI64>(false, dA, dB, m, n, 0, D, total, dOut, &nb, stream);
+      if (st) return st;
+      st = fetch_partials(dOut, nb, &h, stream);
       if (st) return st;
       s128 t;
       if (!combine_checked(h, &t)) {
@@ -213,8 +238,11 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
       }
       *ivalue = (int64_t)t;
     } else {
-      st = (mode == 0) ? launch_comb<kCombF64>(false, dA, dB, m, n, 0, D, total, dOut, &h, stream)
-                       : launch_comb<kCombC128>(false, dA, dB, m, n, 0, D, total, dOut, &h, stream);
+      uint64_t nb = 0;
+      st = (mode == 0) ? enqueue_comb<kCombF64>(false, dA, dB, m, n, 0, D, total, dOut, &nb, stream)
+                       : enqueue_comb<kCombC128>(false, dA, dB, m, n, 0, D, total, dOut, &nb, stream);
+      if (st) return st;
+      st = fetch_partials(dOut, nb, &h, stream);
       if (st) return st;
       double rh = 0, rl = 0, jh = 0, jl = 0;
       combine_float(h, &rh, &rl, &jh, &jl);

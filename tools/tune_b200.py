@@ -35,7 +35,7 @@ def collect(out_path, trials=7):
 
     rng = np.random.default_rng(0)
     res = {}
-    shapes = sorted({(max(1, round(r * n)), n) for n in range(2, 25) for r in RATIOS})
+    shapes = sorted({(max(1, round(r * n)), n) for n in range(2, 35) for r in RATIOS})
     for m, n in shapes:
         a = as_matrix(rng.uniform(-1, 1, (m, n)))
         cell = {}
@@ -44,7 +44,7 @@ def collect(out_path, trials=7):
                 continue
             run_algorithm(a, alg)  # warm-up (module load, allocation)
             ts = []
-            for _ in range(trials):
+            for _ in range(trials if n <= 28 else 3):
                 t = time.perf_counter()
                 run_algorithm(a, alg)
                 ts.append(time.perf_counter() - t)
