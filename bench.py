@@ -161,10 +161,12 @@ def run_engine(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # under torchrun (WORLD_SIZE set) the NCCL path runs even for N = 1
+    distributed = "WORLD_SIZE" in os.environ
     if world != args.gpus and world > 1:
         print(f"warning: WORLD_SIZE={world} != --gpus {args.gpus}", file=sys.stderr)
     torch.cuda.set_device(local)
-    if world > 1:
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2510_03421_b200 as P
     from paper_2510_03421_b200 import _lib, workloads as W
@@ -183,7 +185,7 @@ def run_engine(args):
 
     def step():
         gpu_partial("glynn", a, k0, k1, False, device_out=part, stream=stream.cuda_stream)
-        if world > 1:
+        if distributed:
             dist.all_gather_into_tensor(gathered, part)
         else:
             gathered.copy_(part)
@@ -201,7 +203,7 @@ def run_engine(args):
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.start()
-    if world > 1:
+    if distributed:
         dist.barrier()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -213,12 +215,12 @@ def run_engine(args):
         ev[i][1].record(stream)
         kernel_ms.append(lib.perm_last_kernel_ms())
     torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
     t_ms = sum(s.elapsed_time(e) for s, e in ev)
     t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_ms = float(t.item())
     grid, log2L = _lib.C.c_int(), _lib.C.c_int()
@@ -230,16 +232,16 @@ def run_engine(args):
     achieved = ops_per_launch / (kern_ms * 1e-3)
 
     # ---- e2e through the public API (host numpy input -> Python float) --
-    if world > 1:
+    if distributed:
         dist.barrier()
     e2e_times = []
     for _ in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        v = P.sharded_permanent(a) if world > 1 else P.glynn(a)
+        v = P.sharded_permanent(a) if distributed else P.glynn(a)
         e2e_times.append(time.perf_counter() - t0)
     e2e = torch.tensor([sum(e2e_times)], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if distributed:
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     e2e_value = steps_total * args.steps / float(e2e.item())
 
@@ -291,7 +293,7 @@ def run_engine(args):
             "clocks": clocks,
         }
         print(json.dumps(line))
-    if world > 1:
+    if distributed:
         dist.barrier()
         dist.destroy_process_group()
     return 0
