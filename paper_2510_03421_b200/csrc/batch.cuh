@@ -23,7 +23,10 @@
 
 namespace permb200 {
 
-constexpr int kBatchThreads = 128;
+#ifndef BATCH_THREADS
+#define BATCH_THREADS 32
+#endif
+constexpr int kBatchThreads = BATCH_THREADS;
 
 template <typename T>
 __device__ __forceinline__ void batch_stage(const T* __restrict__ g, T* s, int64_t first, int64_t count, int E,
@@ -307,6 +310,85 @@ __global__ void __launch_bounds__(kBatchThreads) batch_ryser_kernel(const T* __r
     }
     out[first + threadIdx.x] = acc;
   }
+}
+
+// ------------------------------------------------ combinatoric, memoized DP
+// The combinatoric sum over m-permutations (src/_kernels.py:28-56) with its
+// prefix products memoized over column *sets*:
+//   f_1({j}) = a_0j,  f_k(S) = sum_{j in S} a_{k-1,j} f_{k-1}(S \ {j}),
+//   per = sum_{|T| = m-1} f_{m-1}(T) * (R_{m-1} - sum_{j in T} a_{m-1,j}),
+// R_i the row sum.  For very rectangular shapes (m <= 4) this costs
+// sum_k k C(n,k) flops -- 4x10 (C2b): 90 + 120 x 7 = 930 FP64 ops against
+// 1023 x 4 + 385 x 5 for the subset-skipping Ryser -- with every index
+// compile-time (pairs f_2 in registers).  Exact algebra; sums of products.
+template <typename T, int M, int N>
+__device__ T batch_combdp_one(const T* __restrict__ A /* smem, row stride N */) {
+  T acc = Num<T>::zero();
+  if constexpr (M == 1) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc = Num<T>::add(acc, A[j]);
+    return acc;
+  } else {
+    // row sum of the last row
+    T R = Num<T>::zero();
+#pragma unroll
+    for (int j = 0; j < N; ++j) R = Num<T>::add(R, A[(M - 1) * N + j]);
+    if constexpr (M == 2) {
+      // per = sum_i a0i (R1 - a1i)
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc = Num<T>::add(acc, Num<T>::mul(A[i], Num<T>::sub(R, A[N + i])));
+      return acc;
+    } else if constexpr (M == 3) {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = i + 1; j < N; ++j) {
+          const T f2 = Num<T>::add(Num<T>::mul(A[N + i], A[j]), Num<T>::mul(A[N + j], A[i]));
+          const T g = Num<T>::sub(Num<T>::sub(R, A[2 * N + i]), A[2 * N + j]);
+          acc = Num<T>::add(acc, Num<T>::mul(f2, g));
+        }
+      return acc;
+    } else {
+      static_assert(M == 4, "memoized DP kernel covers m <= 4");
+      constexpr int NP = N * (N - 1) / 2;
+      T f2[NP];
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = i + 1; j < N; ++j)
+          f2[i * N - i * (i + 1) / 2 + (j - i - 1)] =
+              Num<T>::add(Num<T>::mul(A[N + i], A[j]), Num<T>::mul(A[N + j], A[i]));
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int j = i + 1; j < N; ++j)
+#pragma unroll
+          for (int k = j + 1; k < N; ++k) {
+            const T fij = f2[i * N - i * (i + 1) / 2 + (j - i - 1)];
+            const T fik = f2[i * N - i * (i + 1) / 2 + (k - i - 1)];
+            const T fjk = f2[j * N - j * (j + 1) / 2 + (k - j - 1)];
+            const T f3 = Num<T>::add(Num<T>::add(Num<T>::mul(A[2 * N + i], fjk), Num<T>::mul(A[2 * N + j], fik)),
+                                     Num<T>::mul(A[2 * N + k], fij));
+            const T g = Num<T>::sub(Num<T>::sub(Num<T>::sub(R, A[3 * N + i]), A[3 * N + j]), A[3 * N + k]);
+            acc = Num<T>::add(acc, Num<T>::mul(f3, g));
+          }
+      return acc;
+    }
+  }
+}
+
+template <typename T, int M, int N>
+__global__ void __launch_bounds__(kBatchThreads) batch_combdp_kernel(const T* __restrict__ a, T* __restrict__ out,
+                                                                     int64_t nbatch) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* s = reinterpret_cast<T*>(smem_raw);
+  constexpr int E = M * N;
+  constexpr int STRIDE = (sizeof(T) == 8) ? (E | 1) : E + 1;
+  const int64_t first = (int64_t)blockIdx.x * kBatchThreads;
+  const int64_t count = (nbatch - first < kBatchThreads) ? nbatch - first : kBatchThreads;
+  batch_stage<T>(a, s, first, count, E, STRIDE);
+  __syncthreads();
+  if (threadIdx.x < count) out[first + threadIdx.x] = batch_combdp_one<T, M, N>(s + threadIdx.x * STRIDE);
 }
 
 // ---------------------------------------------------------------- generic

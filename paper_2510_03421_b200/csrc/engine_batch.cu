@@ -87,6 +87,29 @@ static cudaError_t launch_generic(const void* a, void* out, int64_t B, int m, in
   return cudaGetLastError();
 }
 
+template <typename T, int M, int N>
+static cudaError_t launch_bcombdp(const void* a, void* out, int64_t B, cudaStream_t s) {
+  constexpr int E = M * N;
+  constexpr int STRIDE = (sizeof(T) == 8) ? (E | 1) : E + 1;
+  const size_t smem = (size_t)kBatchThreads * STRIDE * sizeof(T);
+  auto k = batch_combdp_kernel<T, M, N>;
+  cudaError_t e = prep_smem<T>((const void*)k, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = (B + kBatchThreads - 1) / kBatchThreads;
+  k<<<(unsigned)grid, kBatchThreads, smem, s>>>(static_cast<const T*>(a), static_cast<T*>(out), B);
+  return cudaGetLastError();
+}
+// (M, N) with 1 <= M <= 4, M <= N <= 12: IDX = (M-1)*12 + (N-1), N >= M
+template <typename T, int... Is>
+static batch_fn pick_combdp(int m, int n, std::integer_sequence<int, Is...>) {
+  batch_fn f = nullptr;
+  ((m == Is / 12 + 1 && n == Is % 12 + 1 && Is % 12 + 1 >= Is / 12 + 1
+        ? (f = &launch_bcombdp<T, Is / 12 + 1, (Is % 12 + 1 >= Is / 12 + 1 ? Is % 12 + 1 : Is / 12 + 1)>, 0)
+        : 0),
+   ...);
+  return f;
+}
+
 template <typename T, int N>
 static cudaError_t launch_bglynn_warp(const void* a, void* out, int64_t B, cudaStream_t s) {
   const int64_t grid = (B + kBatchWarpMats - 1) / kBatchWarpMats;
@@ -115,6 +138,9 @@ static int launch_batch(int alg, bool cplx, int64_t B, int m, int n, const void*
   if (!fn && alg == PERM_ALG_GLYNN && m == n && n >= 2 && n <= 12)
     fn = cplx ? pick_glynn<cd>(n, std::make_integer_sequence<int, 11>{})
               : pick_glynn<double>(n, std::make_integer_sequence<int, 11>{});
+  if (!fn && alg == PERM_ALG_COMBINATORIC && m <= 4 && n <= 12)
+    fn = cplx ? pick_combdp<cd>(m, n, std::make_integer_sequence<int, 48>{})
+              : pick_combdp<double>(m, n, std::make_integer_sequence<int, 48>{});
   if (!fn && alg == PERM_ALG_RYSER && m < n && n <= 12)
     fn = cplx ? pick_ryser<cd>(m, n, std::make_integer_sequence<int, 66>{})
               : pick_ryser<double>(m, n, std::make_integer_sequence<int, 66>{});
@@ -187,9 +213,10 @@ static void par_memcpy(void* dst, const void* src, size_t bytes) {
 }
 
 int batch_select(int m, int n) {
-  // thread-per-matrix fast paths: Glynn for squares, subset-skipping Ryser
-  // for rectangles (cheapest exact per-matrix work for C2a / C2b)
-  return (m == n) ? PERM_ALG_GLYNN : PERM_ALG_RYSER;
+  // cheapest exact per-matrix work: Glynn for squares, the memoized
+  // combinatoric DP for m <= 4 (C2b: 930 flops), subset-skipping Ryser else
+  if (m == n) return PERM_ALG_GLYNN;
+  return (m <= 4 && n <= 12) ? PERM_ALG_COMBINATORIC : PERM_ALG_RYSER;
 }
 
 int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a, double* out, int dev_ptr,
