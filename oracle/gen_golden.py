@@ -208,6 +208,17 @@ def gen_c4():
     (OUT / "c4.json").write_text(json.dumps(res, indent=1) + "\n")
 
 
+def gen_precision():
+    """The reference's digits-lost table (src/oracles.py:160-236) at
+    --max-n 16 --attempts 200 (SURVEY 8(f) item 2 baseline)."""
+    from permanent.oracles import precision_csv, run_precision_suite
+
+    t = time.time()
+    recs = run_precision_suite(n_range=range(2, 17), seed=0, cauchy_attempts=200)
+    (OUT / "precision_ref.csv").write_text(precision_csv(recs))
+    print(f"precision_ref.csv: {len(recs)} rows, {time.time() - t:.1f}s")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-slow", action="store_true")
@@ -216,7 +227,8 @@ def main():
     OUT.mkdir(parents=True, exist_ok=True)
     O.build()
     steps = {"parity": gen_parity, "ref_cases": gen_ref_cases, "ref_int_walk": gen_ref_int_walk,
-             "c1": gen_c1, "c2": gen_c2, "c3": lambda: gen_c3(args.skip_slow), "c4": gen_c4}
+             "c1": gen_c1, "c2": gen_c2, "c3": lambda: gen_c3(args.skip_slow), "c4": gen_c4,
+             "precision": gen_precision}
     for name, fn in steps.items():
         if args.only and name not in args.only.split(","):
             continue

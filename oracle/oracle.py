@@ -323,9 +323,13 @@ def dd_permanent(alg: str, a, scale=None, nthreads=None):
 
 
 def prescale_factor(a: np.ndarray) -> float:
-    """Power of two k ~ 1/RMS(|a|): the rectangular-Glynn
-    conditioning fix.  Same rule as the engine."""
-    rms = float(np.sqrt(np.mean(np.abs(a) ** 2)))
+    """Power of two k ~ 1/RMS of the nonzero |a_ij|: the
+    rectangular-Glynn conditioning fix.  Same rule as the engine."""
+    mag2 = np.abs(a) ** 2
+    nz = mag2[mag2 != 0]
+    if nz.size == 0:
+        return 1.0
+    rms = float(np.sqrt(np.mean(nz)))
     if not np.isfinite(rms) or rms == 0.0:
         return 1.0
     return float(2.0 ** round(-math.log2(rms)))

@@ -435,13 +435,19 @@ __global__ void __launch_bounds__(kBatchThreads) batch_generic_kernel(const T* _
     }
   } else if (alg == 2) {
     // pre-scale the real rows by k = 2^round(-log2 RMS)
+    // (RMS over the nonzero entries, as prescale_log2 on the host)
     double ss = 0.0;
+    int nz = 0;
     for (int e = 0; e < E; ++e) {
       const double x = Num<T>::re(A[e]), y = Num<T>::im(A[e]);
-      ss += x * x + y * y;
+      const double q = x * x + y * y;
+      if (q != 0.0) {
+        ss += q;
+        ++nz;
+      }
     }
     int sl = 0;
-    if (m < n && ss > 0.0) sl = (int)rint(-0.5 * log2(ss / (double)E));
+    if (m < n && nz > 0) sl = (int)rint(-0.5 * log2(ss / (double)nz));
     T v[16];
     for (int j = 0; j < n; ++j) {
       T c = Num<T>::zero();

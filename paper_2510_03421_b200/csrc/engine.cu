@@ -112,15 +112,22 @@ uint64_t walk_steps(int alg, int m, int n) {
 }
 
 int prescale_log2(const HostMat& A) {
+  // RMS over the nonzero entries: zeros carry no scale (a padded identity
+  // keeps k = 1 and stays exact), dense rows get k ~ 1/|a_ij|
   long double ss = 0;
+  long nz = 0;
   for (int i = 0; i < A.m; ++i)
     for (int j = 0; j < A.n; ++j) {
       long double r = A.re(i, j), im = A.im(i, j);
-      ss += r * r + im * im;
+      const long double q = r * r + im * im;
+      if (q != 0) {
+        ss += q;
+        ++nz;
+      }
     }
-  double rms = std::sqrt((double)(ss / ((long double)A.m * A.n)));
+  if (nz == 0) return 0;
+  double rms = std::sqrt((double)(ss / (long double)nz));
   if (!std::isfinite(rms) || rms == 0.0) return 0;
-  // round half away from zero, as Python's round() differs only on exact .5
   double e = -std::log2(rms);
   double r = std::nearbyint(e);  // ties-to-even, same as Python round()
   return (int)r;

@@ -5,12 +5,16 @@ File format: the reference's (/root/reference/pkg/src/permanent/tuner.py:340-383
 one key per line, floats in shortest round-trip form; unknown, duplicate or
 missing keys and other versions are rejected with ValueError.
 
-The tuner reuses the reference's *procedure* (tuner.py:286-310: time every
-algorithm over an (m, n) grid, label each cell with its fastest algorithm,
-fit the two separating lines and the regime boundary p8) with B200 kernel
-timings in place of CPU timings; the lines are fitted by exhaustive search
-over a parameter grid (minimum total slowdown), a robust stand-in for the
-reference's hard-margin SVM (src/svm.py) when labels are not separable.
+Two fits over B200 kernel timings {(m, n): {alg: seconds}}:
+* ``run_tuning`` -- the reference's procedure (tuner.py:108-310): timing
+  grid, labels with margin ratios, near-tie filter, two maximum-margin lines
+  over (r, n) (hard-margin SVM, weighted minimum-cost fallback when the
+  labels are not separable), p4 from the square cutoff, p8 chosen to
+  minimize the total dispatch slowdown;
+* ``fit_params`` -- a direct grid search minimizing the summed relative
+  slowdown (used for the shipped ``tuned/b200.tuning``: GPU timings below
+  ~50 us are launch-overhead dominated, so labels there are noisy and
+  rarely separable).
 """
 from __future__ import annotations
 
@@ -131,3 +135,257 @@ def fit_params(timings: dict, host: str = "") -> TuningParams:
                                       .strftime("%Y-%m-%dT%H:%M:%SZ"),
                                       host=host or platform.node())
     return best_p
+
+
+# ---------------------------------------------------------------------------
+# The reference's tuning procedure (src/tuner.py:108-310) on B200 timings:
+# timing grid -> labels with margin ratios -> near-tie filter -> two
+# maximum-margin lines over (r, n) -> p4 / p8 -> TuningParams.
+# ---------------------------------------------------------------------------
+import statistics  # noqa: E402
+import time  # noqa: E402
+from dataclasses import dataclass  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+GRID_N = range(2, 35)
+GRID_RATIOS = (1 / 8, 1 / 4, 3 / 8, 1 / 2, 5 / 8, 3 / 4, 7 / 8, 1.0)
+NEAR_TIE_FILTER = 1.05
+COMBINATORIC_MAX_STEPS = 50_000_000
+MIN_SAMPLE_SECONDS = 200e-6
+
+
+@dataclass(frozen=True)
+class BenchmarkSample:
+    algorithm: object
+    m: int
+    n: int
+    ratio: float
+    median_time: float
+    trials: int
+    feasible: bool = True
+
+
+@dataclass(frozen=True)
+class LabeledPoint:
+    r: float
+    n: int
+    m: int
+    label: object
+    margin_ratio: float
+    best_median: float = 0.0
+
+
+@dataclass(frozen=True)
+class SeparatingPlane:
+    weight_r: float
+    weight_n: float
+    bias: float
+    fallback: bool = False
+
+    def evaluate(self, r, n):
+        return self.weight_r * r + self.weight_n * n + self.bias
+
+
+@dataclass(frozen=True)
+class TuningReport:
+    params: TuningParams
+    grid: list
+    plane_small: SeparatingPlane
+    plane_large: SeparatingPlane
+    timings: dict
+
+
+def grid_shapes(n_range=GRID_N, ratios=GRID_RATIOS):
+    seen, out = set(), []
+    for n in n_range:
+        for r in ratios:
+            m = max(1, round(r * n))
+            if m <= n and (m, n) not in seen:
+                seen.add((m, n))
+                out.append((m, n))
+    return out
+
+
+def time_algorithm(alg, m, n, trials=5, seed=None) -> BenchmarkSample:
+    """Median wall time of run_algorithm on fresh U[-1,1] float64 matrices,
+    repeats amortized to >= MIN_SAMPLE_SECONDS (src/tuner.py:108-135)."""
+    from .algorithms import AlgorithmId, run_algorithm
+    from .core import as_matrix
+
+    if trials < 3:
+        raise ValueError(f"need at least 3 trials, got {trials}")
+    if alg is AlgorithmId.COMBINATORIC and math.perm(n, m) > COMBINATORIC_MAX_STEPS:
+        return BenchmarkSample(alg, m, n, m / n, math.inf, 0, feasible=False)
+    g = np.random.default_rng(seed)
+    mats = [as_matrix(g.uniform(-1.0, 1.0, (m, n))) for _ in range(trials + 1)]
+    t0 = time.perf_counter()
+    run_algorithm(mats[0], alg)
+    warm = time.perf_counter() - t0
+    reps = max(1, min(200, round(MIN_SAMPLE_SECONDS / max(warm, 1e-9))))
+    ts = []
+    for mat in mats[1:]:
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            run_algorithm(mat, alg)
+        ts.append((time.perf_counter() - t0) / reps)
+    return BenchmarkSample(alg, m, n, m / n, statistics.median(ts), trials)
+
+
+def label_grid(timings: dict) -> list:
+    """Label each cell {(m, n): {alg: seconds}} by its fastest algorithm."""
+    from .algorithms import AlgorithmId
+
+    pts = []
+    for (m, n), t in sorted(timings.items(), key=lambda kv: (kv[0][1], kv[0][0])):
+        feas = sorted((v, a) for a, v in t.items() if math.isfinite(v))
+        if not feas:
+            continue
+        margin = feas[1][0] / feas[0][0] if len(feas) > 1 else math.inf
+        pts.append(LabeledPoint(m / n, n, m, AlgorithmId(feas[0][1]), margin, feas[0][0]))
+    return pts
+
+
+def build_label_grid(n_range=GRID_N, ratios=GRID_RATIOS, trials=5, seed=0):
+    from .algorithms import AlgorithmId
+
+    timings, s = {}, seed
+    for m, n in grid_shapes(n_range, ratios):
+        cell = {}
+        for alg in AlgorithmId:
+            s += 1
+            smp = time_algorithm(alg, m, n, trials=trials, seed=s)
+            if smp.feasible:
+                cell[alg.value] = smp.median_time
+        timings[(m, n)] = cell
+    return label_grid(timings), timings
+
+
+def detect_small_square_cutoff(grid) -> int:
+    """Largest n with combinatoric fastest on every square up to n (else 1)."""
+    from .algorithms import AlgorithmId
+
+    cut = 1
+    for p in sorted((p for p in grid if p.m == p.n and p.n >= 2), key=lambda p: p.n):
+        if p.label is not AlgorithmId.COMBINATORIC:
+            break
+        cut = p.n
+    return cut
+
+
+def _max_margin(X, y):
+    """Hard-margin linear SVM in 2-D (min |w|^2 s.t. y (w.x + b) >= 1), or
+    None if the classes are not linearly separable."""
+    from scipy.optimize import minimize
+
+    scale = np.maximum(np.abs(X).max(axis=0), 1e-12)
+    Xs = X / scale
+    cons = {"type": "ineq", "fun": lambda z: y * (Xs @ z[:2] + z[2]) - 1.0,
+            "jac": lambda z: np.column_stack([y[:, None] * Xs, y])}
+    best = None
+    for z0 in (np.array([1.0, 0.0, 0.0]), np.array([0.0, 1.0, 0.0]), np.array([1.0, 1.0, -1.0])):
+        r = minimize(lambda z: z[0] ** 2 + z[1] ** 2, z0, jac=lambda z: np.array([2 * z[0], 2 * z[1], 0.0]),
+                     constraints=[cons], method="SLSQP", options={"maxiter": 500, "ftol": 1e-12})
+        if r.success and np.all(y * (Xs @ r.x[:2] + r.x[2]) >= 1.0 - 1e-6):
+            if best is None or r.fun < best.fun:
+                best = r
+    if best is None:
+        return None
+    w = best.x[:2] / scale
+    return w, float(best.x[2])
+
+
+def _min_cost_line(X, y, weights, angles=1440):
+    """Weighted minimum-misclassification line: sweep directions; for each,
+    the best threshold over sorted projections by cumulative sums."""
+    scale = np.maximum(np.abs(X).max(axis=0), 1e-12)
+    Xs = X / scale
+    best = (math.inf, None, None)
+    for th in np.linspace(0.0, 2 * math.pi, angles, endpoint=False):
+        w = np.array([math.cos(th), math.sin(th)])
+        proj = Xs @ w
+        order = np.argsort(proj)
+        ps, ys, ws = proj[order], y[order], weights[order]
+        # threshold after position i: points <= are predicted -1, > are +1
+        pos_left = np.concatenate([[0.0], np.cumsum(ws * (ys > 0))])       # +1 points on the -1 side
+        neg_right = np.concatenate([np.cumsum((ws * (ys < 0))[::-1])[::-1], [0.0]])  # -1 points on the +1 side
+        cost = pos_left + neg_right
+        i = int(np.argmin(cost))
+        if cost[i] < best[0]:
+            if i == 0:
+                b = ps[0] - 1.0
+            elif i == len(ps):
+                b = ps[-1] + 1.0
+            else:
+                b = 0.5 * (ps[i - 1] + ps[i])
+            best = (float(cost[i]), w / scale, -b)
+    return best[1], best[2]
+
+
+def fit_separator(points, class_a, class_b, near_tie=NEAR_TIE_FILTER) -> SeparatingPlane:
+    """Max-margin line between two labels over (r, n) after the near-tie
+    filter; weighted min-cost fallback when not separable (src/tuner.py:187-213)."""
+    kept = [p for p in points if p.label in (class_a, class_b) and p.margin_ratio >= near_tie]
+    if not any(p.label is class_a for p in kept) or not any(p.label is class_b for p in kept):
+        raise ValueError("both classes need retained training points")
+    X = np.array([[p.r, p.n] for p in kept], dtype=float)
+    y = np.array([1.0 if p.label is class_a else -1.0 for p in kept])
+    fit = _max_margin(X, y)
+    if fit is not None:
+        w, b = fit
+        return SeparatingPlane(float(w[0]), float(w[1]), b)
+    wts = np.array([min(p.margin_ratio, 10.0) - 1.0 for p in kept])
+    w, b = _min_cost_line(X, y, wts)
+    return SeparatingPlane(float(w[0]), float(w[1]), float(b), fallback=True)
+
+
+def _total_slowdown(params, timings):
+    from .dispatch import select_algorithm
+
+    tot = 0.0
+    for (m, n), t in timings.items():
+        pick = select_algorithm(m, n, params).value
+        tot += (t[pick] / min(t.values())) if pick in t else 1e6
+    return tot
+
+
+def run_tuning(n_range=GRID_N, ratios=GRID_RATIOS, trials=5, seed=0, timings=None) -> TuningReport:
+    """The whole pipeline; with ``timings`` ({(m, n): {alg: s}}) it only fits."""
+    import datetime
+    import platform
+
+    from .algorithms import AlgorithmId
+
+    C, G, R = AlgorithmId.COMBINATORIC, AlgorithmId.GLYNN, AlgorithmId.RYSER
+    if timings is None:
+        grid, timings = build_label_grid(n_range, ratios, trials, seed)
+    else:
+        grid = label_grid(timings)
+    max_n = max(p.n for p in grid)
+    p4 = detect_small_square_cutoff(grid)
+
+    def plane(pts, a, b, default):
+        try:
+            return fit_separator(pts, a, b)
+        except ValueError:
+            return default
+
+    plane1 = plane([p for p in grid if not (p.m == p.n and p.n <= p4)], C, G,
+                   SeparatingPlane(-1.0, 0.0, -1.0, fallback=True))
+    best = None
+    for p8 in range(max(2, p4), max_n + 1):
+        large = [p for p in grid if p.n > p8]
+        plane2 = plane(large or grid, G, R, SeparatingPlane(1.0, 0.0, 1.0, fallback=True))
+        try:
+            params = TuningParams(plane1.weight_r, plane1.weight_n, plane1.bias, float(p4),
+                                  plane2.weight_r, plane2.weight_n, plane2.bias, float(p8),
+                                  source="machine-tuned")
+        except ValueError:
+            continue
+        cost = _total_slowdown(params, timings)
+        if best is None or cost < best[0]:
+            best = (cost, params, plane2)
+    _, params, plane2 = best
+    stamp = datetime.datetime.now(datetime.timezone.utc).strftime("%Y-%m-%dT%H:%M:%SZ")
+    params = TuningParams(*params.as_list(), source="machine-tuned", created_at=stamp, host=platform.node())
+    return TuningReport(params, grid, plane1, plane2, timings)

@@ -1,0 +1,113 @@
+"""Host-side parts of the precision suite, CLI and tuner (no GPU): analytic
+truths, digits-lost, CSV, matrix text parsing / formatting / exit codes for
+bad input, and the tuning pipeline's fit on synthetic timings.  Mirrors the
+reference's pkg/tests/test_oracles.py, test_cli.py and test_tuner.py."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2510_03421_b200 import cli, precision as PR, tuning as T
+from paper_2510_03421_b200.algorithms import AlgorithmId
+from paper_2510_03421_b200.core import ElementKind
+from paper_2510_03421_b200.dispatch import select_algorithm
+
+
+# --------------------------------------------------------------- precision
+def test_analytic_truths():
+    assert PR.ones_permanent(3, 5) == 60
+    assert PR.ones_permanent(20, 25) == float(math.perm(25, 20))
+    assert PR.identity_permanent(3, 7) == 1
+    with pytest.raises(ValueError):
+        PR.ones_permanent(4, 3)
+    assert PR.identity_matrix(2, 4).data.tolist() == [[1.0, 0, 0, 0], [0, 1.0, 0, 0]]
+    assert PR.ones_matrix(2, 3, ElementKind.INT64).kind is ElementKind.INT64
+
+
+def test_borchardt_matches_bruteforce():
+    for n in (3, 5, 7):
+        spec = PR.sample_cauchy(n, attempts=20, seed=n)
+        exact = O.brute_force((1.0 / np.add.outer(spec.x, spec.y)).tolist())
+        assert PR.borchardt_permanent(spec) == pytest.approx(exact, rel=1e-9)
+    a = PR.sample_cauchy(6, attempts=30, seed=1)
+    b = PR.sample_cauchy(6, attempts=30, seed=1)
+    assert np.array_equal(a.x, b.x) and a.condition == b.condition
+
+
+def test_digits_lost_and_csv():
+    assert PR.digits_lost(1.0, 1.0) == PR.FLOOR_SENTINEL
+    assert PR.digits_lost(1.0 + 1e-13, 1.0) == pytest.approx(math.log10(1e-13) - math.log10(PR.MACHEPS), abs=1e-3)
+    with pytest.raises(ValueError):
+        PR.digits_lost(1.0, 0)
+    recs = [PR.PrecisionRecord("ones", AlgorithmId.GLYNN, 2, 3, ElementKind.FLOAT64, 0.5, False),
+            PR.PrecisionRecord("ones", AlgorithmId.RYSER, 2, 3, ElementKind.INT64, None, True)]
+    text = PR.precision_csv(recs)
+    assert text.splitlines() == ["family,algorithm,m,n,kind,digits_lost,overflow",
+                                 "ones,glynn,2,3,float64,0.5,false", "ones,ryser,2,3,int64,,true"]
+    with pytest.raises(ArithmeticError):
+        PR.det_partial_pivot(np.ones((3, 3)))
+
+
+# ---------------------------------------------------------------------- CLI
+def test_parse_and_format():
+    m = cli.parse_matrix_text("1 2; 3 4")
+    assert m.kind is ElementKind.INT64 and m.tolist() == [[1, 2], [3, 4]]
+    assert cli.parse_matrix_text("1 2.5\n3 4").kind is ElementKind.FLOAT64
+    assert cli.parse_matrix_text("1+2i 0; 0 1").kind is ElementKind.COMPLEX128
+    assert cli.parse_matrix_text("1e3 1").tolist() == [[1000.0, 1.0]]
+    for bad in ("", "1 2; 3", "1 x"):
+        with pytest.raises(ValueError):
+            cli.parse_matrix_text(bad)
+    assert cli.format_value(450) == "450"
+    assert cli.format_value(0.5) == "5.e-01"
+    assert cli.format_value(complex(1.5, -2.0)) == "1.5e+00-2.e+00i"
+
+
+def test_cli_exit_codes_for_bad_input(capsys, tmp_path):
+    assert cli.main(["compute", "1 2; 3"]) == 2
+    assert cli.main(["compute", "--algorithm", "glynn_square", "1 2 3; 4 5 6"]) == 2
+    assert cli.main(["compute", "--algorithm", "glynn_rectangular", "1 2; 3 4"]) == 2
+    assert cli.main(["compute", "--input", str(tmp_path / "missing.txt")]) == 4
+    with pytest.raises(SystemExit):
+        cli.main(["compute", "--algorithm", "bogus", "1"])
+
+
+# -------------------------------------------------------------------- tuner
+def synthetic_timings():
+    """Cost-model timings: C ~ P(n,m), G ~ 2^(n-1) n, R ~ 2^n m (+ launch floor)."""
+    t = {}
+    for m, n in T.grid_shapes(range(2, 25)):
+        cell = {"glynn": 4e-5 + 2 ** (n - 1) * 2 * n / 1.5e13,
+                "ryser": 4e-5 + 2 ** n * 2 * m / 1.5e13}
+        if math.perm(n, m) <= T.COMBINATORIC_MAX_STEPS:
+            cell["combinatoric"] = 3e-5 + math.perm(n, m) * m / 2e12
+        t[(m, n)] = cell
+    return t
+
+
+def test_tuning_pipeline_on_synthetic_timings():
+    t = synthetic_timings()
+    rep = T.run_tuning(timings=t)
+    p = rep.params
+    assert p.source == "machine-tuned"
+    # the max-margin table is close to (or better than) the defaults here
+    from paper_2510_03421_b200.dispatch import default_params
+
+    assert T._total_slowdown(p, t) <= 1.02 * T._total_slowdown(default_params(), t)
+    grid = T.label_grid(t)
+    assert all(pt.margin_ratio >= 1.0 for pt in grid)
+    for (m, n) in t:
+        select_algorithm(m, n, p)  # total over the grid
+
+
+def test_max_margin_separates():
+    X = np.array([[0.1, 2], [0.2, 3], [0.9, 20], [0.8, 22]], dtype=float)
+    y = np.array([1.0, 1.0, -1.0, -1.0])
+    w, b = T._max_margin(X, y)
+    assert np.all(y * (X @ w + b) > 0)
+    wts = np.ones(4)
+    w2, b2 = T._min_cost_line(X, y, wts)
+    assert np.all(y * (X @ w2 + b2) > 0)
