@@ -186,6 +186,69 @@ static int checked_walk(const IntSetup& s, cudaStream_t stream, bool* ovf, int64
 
 // ------------------------------------------------------------ WRAP walk
 walk_fn_i int_wrap_lookup(int P);
+walk_fn_if int_wrap_fp_lookup(int P);
+
+// Fused path: FP64-exact state and group products (|state| <= 98), the
+// int128 sum and its FP64 estimate / magnitude sum from one kernel.
+static bool fp_walk_ok(const IntSetup& s) {
+  return !s.weighted && s.bound <= 98 && s.B >= 8 && s.P >= 1 && s.P <= 64;
+}
+
+static int wrap_walk_fp(const IntSetup& s, cudaStream_t stream, s128* raw, long double* est, long double* mag) {
+  const uint64_t steps = 1ull << s.B;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t lanes = (uint64_t)nsm * 8 * kIntThreads;
+  int log2L = 3;
+  while (log2L < 14 && (steps >> (log2L + 1)) >= 16 * lanes) ++log2L;
+  const uint64_t nchunks = steps >> log2L;
+  const uint64_t blocks = std::min<uint64_t>((nchunks + kIntThreads - 1) / kIntThreads, (uint64_t)nsm * 8);
+  std::vector<double> buf(s.v0.size() + s.U.size());
+  for (size_t i = 0; i < s.v0.size(); ++i) buf[i] = (double)s.v0[i];
+  for (size_t i = 0; i < s.U.size(); ++i) buf[s.v0.size() + i] = (double)s.U[i];
+  const size_t bytes = buf.size() * 8 + blocks * 64 + 256;
+  DevBuf dbuf;
+  PERM_CUDA_TRY(cudaMallocAsync(&dbuf.p, bytes, stream));
+  double* d = static_cast<double*>(dbuf.p);
+  PERM_CUDA_TRY(cudaMemcpyAsync(d, buf.data(), buf.size() * 8, cudaMemcpyHostToDevice, stream));
+  IntWalkFArgs a;
+  a.v0 = d;
+  a.U = d + s.v0.size();
+  a.P = s.P;
+  a.B = s.B;
+  a.log2L = log2L;
+  a.k_begin = 0;
+  a.nchunks = nchunks;
+  a.out = reinterpret_cast<int64_t*>(d + buf.size());
+  walk_fn_if fn = int_wrap_fp_lookup(s.P);
+  if (!fn) {
+    set_error("no fp int walk for this size");
+    return PERM_BAD_SHAPE;
+  }
+  PERM_CUDA_TRY(fn(a, (int)blocks, stream));
+  std::vector<int64_t> h(blocks * 8);
+  PERM_CUDA_TRY(cudaMemcpyAsync(h.data(), a.out, blocks * 64, cudaMemcpyDeviceToHost, stream));
+  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  PERM_CUDA_TRY(cudaFreeAsync(dbuf.p, stream));
+  dbuf.p = nullptr;
+  unsigned __int128 acc = 0;
+  double H = 0, L = 0, M = 0;
+  for (uint64_t b = 0; b < blocks; ++b) {
+    const int64_t* o = &h[b * 8];
+    acc += ((unsigned __int128)(uint64_t)o[1] << 64) | (uint64_t)o[0];
+    double hh, ll, mm;
+    std::memcpy(&hh, &o[2], 8);
+    std::memcpy(&ll, &o[3], 8);
+    std::memcpy(&mm, &o[4], 8);
+    dd_add(H, L, hh, ll);
+    M += mm;
+  }
+  *raw = (s128)acc;
+  *est = (long double)H + (long double)L;
+  *mag = M;
+  return PERM_OK;
+}
 
 static int wrap_walk(const IntSetup& s, cudaStream_t stream, s128* raw) {
   const bool wide = s.bound >= ((s128)1 << 62);  // int64 state could wrap
@@ -346,6 +409,36 @@ int int_permanent(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_
   }
   const long double apriori = (m == n ? std::min(rows, cols) : rows) * (long double)denom;
   const bool cert_apriori = apriori < std::ldexp(1.0L, 126);
+  if (fp_walk_ok(s)) {
+    // one pass: exact int128 walk + its own FP64 estimate.  Error of the
+    // estimate of the raw sum: <= 3 product roundings per term (group
+    // products are exact) and chunk sums of <= 2^14 terms, i.e.
+    // E <= (3 + 2^14 + 16) u M_raw.
+    s128 raw = 0;
+    long double est = 0, mag_raw = 0;
+    st = wrap_walk_fp(s, stream, &raw, &est, &mag_raw);
+    if (st) return st;
+    const long double E = (long double)(3 + (1 << 14) + 16) * std::ldexp(1.0L, -52) * mag_raw;
+    if (!cert_apriori && std::fabs(est) + E >= std::ldexp(1.0L, 126)) {
+      set_error("exact value not certified to fit the int128 walk");
+      return PERM_OVERFLOW;
+    }
+    if (std::fabs((long double)raw - est) > E + 1.0L) {
+      set_error("internal: int128 walk disagrees with its FP64 estimate");
+      return PERM_CUDA;
+    }
+    s128 v = raw;
+    if (alg == PERM_ALG_GLYNN) {
+      if (v % denom != 0) {
+        set_error("internal: Glynn int128 sum not divisible by its normalization");
+        return PERM_CUDA;
+      }
+      v /= denom;
+    } else if (m == n && (n & 1)) {
+      v = -v;
+    }
+    return to_out(v, out, fits_int64);
+  }
   double per_fp = 0, mag = 0;
   if (!cert_apriori) {
     if (s.bound >= ((s128)1 << 52)) {

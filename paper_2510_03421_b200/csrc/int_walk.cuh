@@ -18,6 +18,7 @@
 // host certifies with an FP64 run plus its magnitude-sum error bound.
 #pragma once
 #include "common.cuh"
+#include "walk.cuh"
 
 namespace permb200 {
 
@@ -351,7 +352,137 @@ __global__ void __launch_bounds__(kIntThreads) int_walk_wrap_kernel(IntWalkArgs 
   }
 }
 
+// FP64-exact WRAP walk for small integer entries (|state| <= 98, so a
+// product of 8 state entries is < 2^53): state updates and group products
+// run on the FP64 pipe exactly, each group product is converted to int64
+// and folded into the mod-2^128 term.  The same products give the FP64
+// estimate of every term for free, so the int128 fit certificate (FP64 sum
+// + magnitude sum) is accumulated in the same pass.  Per block out slots:
+// [0..1] int128 sum, [2..3] FP64 double-double sum, [4] magnitude sum.
+struct IntWalkFArgs {
+  const double* v0;   // [P] exact integers
+  const double* U;    // [B][P] exact integers
+  int P, B, log2L;
+  uint64_t k_begin, nchunks;
+  int64_t* out;       // [blocks][8]
+};
+
+template <int P>
+__device__ __forceinline__ void fp_term(const double (&v)[P], bool neg, i128& acc, double& est, double& mag) {
+  constexpr int NG = (P + 7) / 8;
+  double g[NG];
+#pragma unroll
+  for (int q = 0; q < NG; ++q) {
+    double x = v[8 * q];
+#pragma unroll
+    for (int j = 8 * q + 1; j < 8 * q + 8 && j < P; ++j) x *= v[j];
+    g[q] = x;
+  }
+  i128 p = i128_from(__double2ll_rn(g[0]));
+  double f = g[0];
+#pragma unroll
+  for (int q = 1; q < NG; ++q) {
+    p = i128_mul_s64(p, __double2ll_rn(g[q]));
+    f *= g[q];
+  }
+  if (neg) {
+    acc = i128_sub(acc, p);
+    est -= f;
+  } else {
+    acc = i128_add(acc, p);
+    est += f;
+  }
+  mag += fabs(f);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kIntThreads) int_walk_wrap_fp_kernel(IntWalkFArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sU = reinterpret_cast<double*>(smem_raw);
+  constexpr int PS = (P + 1) & ~1;
+  const int B = a.B;
+  for (int i = threadIdx.x; i < B * P; i += kIntThreads) sU[(i / P) * PS + (i % P)] = a.U[i];
+  __syncthreads();
+  const uint64_t nq = (1ull << a.log2L) >> 3;
+  i128 acc = i128_from(0);
+  double hi = 0.0, lo = 0.0, mag = 0.0;
+  const uint64_t nthr = (uint64_t)gridDim.x * kIntThreads;
+  for (uint64_t c = (uint64_t)blockIdx.x * kIntThreads + threadIdx.x; c < a.nchunks; c += nthr) {
+    const uint64_t k0 = a.k_begin + (c << a.log2L);
+    double v[P];
+    const uint64_t g0 = k0 ^ (k0 >> 1);
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = a.v0[j];
+    for (int t = 0; t < B; ++t)
+      if ((g0 >> t) & 1) row_add<double, P>(v, sU + t * PS);
+    double est = 0.0;
+    for (uint64_t q = 0; q < nq; ++q) {
+      const uint64_t l0 = q << 3;
+      if (q) {
+        const int t = __ffsll((long long)l0) - 1;
+        const uint64_t k = k0 + l0;
+        const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
+        row_fma<double, P>(v, set ? 1.0 : -1.0, sU + t * PS);
+      }
+      fp_term<P>(v, false, acc, est, mag);
+      row_add<double, P>(v, sU);
+      fp_term<P>(v, true, acc, est, mag);
+      row_add<double, P>(v, sU + PS);
+      fp_term<P>(v, false, acc, est, mag);
+      row_sub<double, P>(v, sU);
+      fp_term<P>(v, true, acc, est, mag);
+      row_fma<double, P>(v, (((k0 + l0) >> 3) & 1) ? -1.0 : 1.0, sU + 2 * PS);
+      fp_term<P>(v, false, acc, est, mag);
+      row_add<double, P>(v, sU);
+      fp_term<P>(v, true, acc, est, mag);
+      row_sub<double, P>(v, sU + PS);
+      fp_term<P>(v, false, acc, est, mag);
+      row_sub<double, P>(v, sU);
+      fp_term<P>(v, true, acc, est, mag);
+    }
+    dd_acc(hi, lo, est);
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    acc = i128_add(acc, shfl_down_i128(acc, off));
+    dd_add(hi, lo, __shfl_down_sync(0xffffffffu, hi, off), __shfl_down_sync(0xffffffffu, lo, off));
+    mag += __shfl_down_sync(0xffffffffu, mag, off);
+  }
+  __shared__ i128 ws[kIntWarps];
+  __shared__ double wd[kIntWarps][3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    ws[warp] = acc;
+    wd[warp][0] = hi; wd[warp][1] = lo; wd[warp][2] = mag;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i128 t = ws[0];
+    double H = wd[0][0], L = wd[0][1], M = wd[0][2];
+    for (int w = 1; w < kIntWarps; ++w) {
+      t = i128_add(t, ws[w]);
+      dd_add(H, L, wd[w][0], wd[w][1]);
+      M += wd[w][2];
+    }
+    int64_t* o = a.out + (size_t)blockIdx.x * 8;
+    o[0] = (int64_t)t.lo; o[1] = (int64_t)t.hi;
+    o[2] = __double_as_longlong(H); o[3] = __double_as_longlong(L); o[4] = __double_as_longlong(M);
+  }
+}
+
 using walk_fn_i = cudaError_t (*)(const IntWalkArgs&, int blocks, cudaStream_t);
+using walk_fn_if = cudaError_t (*)(const IntWalkFArgs&, int blocks, cudaStream_t);
+
+template <int P>
+cudaError_t launch_int_wrap_fp(const IntWalkFArgs& a, int blocks, cudaStream_t stream) {
+  const size_t smem = (size_t)a.B * ((P + 1) & ~1) * sizeof(double);
+  auto kern = int_walk_wrap_fp_kernel<P>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<blocks, kIntThreads, smem, stream>>>(a);
+  return cudaGetLastError();
+}
 
 template <int P>
 cudaError_t launch_int_wrap(const IntWalkArgs& a, int blocks, cudaStream_t stream) {
