@@ -188,10 +188,10 @@ static int checked_walk(const IntSetup& s, cudaStream_t stream, bool* ovf, int64
 walk_fn_i int_wrap_lookup(int P);
 walk_fn_if int_wrap_fp_lookup(int P);
 
-// Fused path: FP64-exact state and group products (|state| <= 98), the
+// Fused path: FP64-exact state and group products (|state| <= 83), the
 // int128 sum and its FP64 estimate / magnitude sum from one kernel.
 static bool fp_walk_ok(const IntSetup& s) {
-  return !s.weighted && s.bound <= 98 && s.B >= 8 && s.P >= 1 && s.P <= 64;
+  return !s.weighted && s.bound <= 83 && s.B >= 8 && s.P >= 1 && s.P <= 64;
 }
 
 static int wrap_walk_fp(const IntSetup& s, cudaStream_t stream, s128* raw, long double* est, long double* mag) {

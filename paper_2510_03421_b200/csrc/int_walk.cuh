@@ -352,8 +352,8 @@ __global__ void __launch_bounds__(kIntThreads) int_walk_wrap_kernel(IntWalkArgs 
   }
 }
 
-// FP64-exact WRAP walk for small integer entries (|state| <= 98, so a
-// product of 8 state entries is < 2^53): state updates and group products
+// FP64-exact WRAP walk for small integer entries (|state| <= 83, so a
+// product of 8 state entries is < 2^51): state updates and group products
 // run on the FP64 pipe exactly, each group product is converted to int64
 // and folded into the mod-2^128 term.  The same products give the FP64
 // estimate of every term for free, so the int128 fit certificate (FP64 sum
@@ -367,6 +367,13 @@ struct IntWalkFArgs {
   int64_t* out;       // [blocks][8]
 };
 
+// Exact double -> int64 for integer values |x| < 2^51 without F2I (whose
+// variable latency stalled the walk on the short scoreboard): adding
+// 1.5 * 2^52 puts x in the low mantissa bits.
+__device__ __forceinline__ int64_t exact_d2ll(double x) {
+  return __double_as_longlong(x + 6755399441055744.0) - 0x4338000000000000LL;
+}
+
 template <int P>
 __device__ __forceinline__ void fp_term(const double (&v)[P], bool neg, i128& acc, double& est, double& mag) {
   constexpr int NG = (P + 7) / 8;
@@ -378,11 +385,11 @@ __device__ __forceinline__ void fp_term(const double (&v)[P], bool neg, i128& ac
     for (int j = 8 * q + 1; j < 8 * q + 8 && j < P; ++j) x *= v[j];
     g[q] = x;
   }
-  i128 p = i128_from(__double2ll_rn(g[0]));
+  i128 p = i128_from(exact_d2ll(g[0]));
   double f = g[0];
 #pragma unroll
   for (int q = 1; q < NG; ++q) {
-    p = i128_mul_s64(p, __double2ll_rn(g[q]));
+    p = i128_mul_s64(p, exact_d2ll(g[q]));
     f *= g[q];
   }
   if (neg) {
@@ -396,7 +403,7 @@ __device__ __forceinline__ void fp_term(const double (&v)[P], bool neg, i128& ac
 }
 
 template <int P>
-__global__ void __launch_bounds__(kIntThreads) int_walk_wrap_fp_kernel(IntWalkFArgs a) {
+__global__ void __launch_bounds__(kIntThreads, 3) int_walk_wrap_fp_kernel(IntWalkFArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* sU = reinterpret_cast<double*>(smem_raw);
   constexpr int PS = (P + 1) & ~1;

@@ -371,3 +371,28 @@ def test_c5_glynn_vs_dd_ryser_n36():
     assert rel_err(g, r) <= 1e-12          # the two dd walks agree
     assert scaled_err(v, r, M) <= TOL      # metric (ii) vs dd Ryser
     assert rel_err(v, r) <= 1e-9           # plain relative error, reported
+
+
+def test_sharded_nccl_single_rank():
+    """The NCCL code path of sharded_permanent (world of one GPU here: the
+    partial stays on the device and goes through all_gather_into_tensor)."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        for a in (W.c5(26), W.c3a(), W.c3b()[:16, :22]):
+            v = P.sharded_permanent(a)
+            ref = P.glynn(a)
+            assert v == pytest.approx(ref, rel=1e-12)
+        v, M = P.sharded_permanent(W.c5(24), alg="ryser", mag=True)
+        assert v == pytest.approx(P.ryser(W.c5(24)), rel=1e-9) and M > 0
+    finally:
+        dist.destroy_process_group()
