@@ -396,3 +396,40 @@ def test_sharded_nccl_single_rank():
         assert v == pytest.approx(P.ryser(W.c5(24)), rel=1e-9) and M > 0
     finally:
         dist.destroy_process_group()
+
+
+def test_permanent_reference_entry_point():
+    """permanent_reference keeps the reference's contract (src/reference.py:136-156)."""
+    from paper_2510_03421_b200.algorithms import StepBudgetExceeded
+
+    two = as_matrix([[1, 2], [3, 4]])
+    assert P.permanent_reference(two, AlgorithmId.RYSER).value == 10
+    assert P.permanent_reference(as_matrix(np.eye(3, dtype=np.int64)), AlgorithmId.GLYNN).value == 1
+    assert P.permanent_reference(as_matrix(np.ones((2, 3), dtype=np.int64)), AlgorithmId.RYSER).value == 6
+    big = as_matrix(np.array([[2**62, 3], [5, 2**62]], dtype=np.int64))
+    r = P.permanent_reference(big, AlgorithmId.COMBINATORIC)
+    assert r.value == 2**124 + 15 and r.overflowed
+    f = np.random.default_rng(3).uniform(-1, 1, (6, 8))
+    assert P.permanent_reference(as_matrix(f), AlgorithmId.GLYNN).value == pytest.approx(
+        O.brute_force(f.tolist()), rel=1e-12)
+    with pytest.raises(StepBudgetExceeded):
+        P.permanent_reference(as_matrix(np.ones((21, 21))), AlgorithmId.RYSER)
+    with pytest.raises(ValueError):
+        P.permanent_reference(as_matrix(np.ones((3, 2))), AlgorithmId.RYSER)
+
+
+def test_concurrent_calls_from_threads():
+    """Re-entrancy: ctypes drops the GIL, each host thread has
+    its own scratch and per-thread stream."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(21)
+    mats = [rng.uniform(-1, 1, (n, n)) for n in (18, 20, 22, 19, 21, 23, 17, 24)]
+    serial = [P.glynn(a) for a in mats]
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        par = list(ex.map(P.glynn, mats))
+    assert par == serial  # deterministic launch shapes -> bit-identical
+    ints = [rng.integers(0, 2, (16, 16)).astype(np.int64) for _ in range(6)]
+    with ThreadPoolExecutor(max_workers=3) as ex:
+        got = list(ex.map(lambda b: P.ryser(b, exact="int128"), ints))
+    assert got == [O.exact_int128("glynn", b) for b in ints]
