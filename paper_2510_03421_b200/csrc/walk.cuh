@@ -152,6 +152,29 @@ __host__ __device__ constexpr int row_stride() { return (sizeof(T) == 8) ? ((P +
 #define WALK_CHAINS 4
 #endif
 constexpr int kChains = WALK_CHAINS;
+// Per-state-length chain count from a measured sweep on B200
+// (tools/walk_csweep.cu, profiles/r1_chain_sweep.txt): ptxas schedules some
+// lengths markedly better with a different chain count (P = 29, 30, 34: +6%).
+// Only changes worth >= 2% are kept; WALK_CHAINS (default 4) elsewhere.
+template <typename T, int P>
+__host__ __device__ constexpr int walk_chains() {
+#ifdef WALK_CHAINS_FIXED
+  return kChains;
+#else
+  if constexpr (sizeof(T) == 8) {
+    switch (P) {
+      case 27: case 40: case 44: return 2;
+      case 31: case 37: return 3;
+      case 34: return 5;
+      case 38: return 6;
+      case 29: case 30: return 8;
+      default: return kChains;
+    }
+  } else {
+    return P == 22 ? 6 : kChains;
+  }
+#endif
+}
 #ifndef WALK_FUSED
 #define WALK_FUSED 1
 #endif
@@ -175,7 +198,8 @@ __device__ __forceinline__ T tree_of(const T (&c)[N]) {
 }
 template <typename T, int P>
 __device__ __forceinline__ T chain_product(const T (&v)[P]) {
-  constexpr int C = (P < kChains) ? P : kChains;
+  constexpr int K = walk_chains<T, P>();
+  constexpr int C = (P < K) ? P : K;
   T c[C];
 #pragma unroll
   for (int i = 0; i < C; ++i) c[i] = v[i];
@@ -217,7 +241,8 @@ struct Term {
 template <typename T, int P, bool W, bool MAG, int UPD>
 __device__ __forceinline__ void term_update(T (&v)[P], const T* __restrict__ row, double s, int sign, int pc,
                                             const double* sW, T& acc, double& mag) {
-  constexpr int C = (P < kChains) ? P : kChains;
+  constexpr int K = walk_chains<T, P>();
+  constexpr int C = (P < K) ? P : K;
   T c[C];
   auto upd = [&](T x, T u) -> T {
     if constexpr (UPD == 0) return Num<T>::add(x, u);

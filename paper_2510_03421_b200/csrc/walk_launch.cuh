@@ -16,6 +16,7 @@ struct WalkJob {
   int wlen;
   int mag;
   uint64_t k_begin, k_end;  // Gray range; k_begin, k_end multiples of 32*L (or tiny range)
+  int force_log2L = 0;       // tuning / test knob: chunk length exponent (0 = cost model)
   double* partials;      // device scratch, >= max_partials() * kPartialStride doubles
 };
 
@@ -79,7 +80,7 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
   if (bps * nsm > kMaxPartials) bps = kMaxPartials / nsm;
   const uint64_t lanes = (uint64_t)bps * nsm * kWalkThreads;
   // alignment: chunks of L must tile [k_begin, k_end) in groups of 32
-  int r = choose_log2L(steps, lanes);
+  int r = job.force_log2L > 0 ? job.force_log2L : choose_log2L(steps, lanes);
   const int amax = std::min(align_log2(job.k_begin), align_log2(steps)) - 5;
   if (r > amax) r = amax;
   if (r < 3 || (steps >> r) < 32) {
