@@ -174,6 +174,7 @@ def run_engine(args):
 
     lib = _lib.load()
     _lib.check(lib.perm_set_device(local), "set_device")
+    lib.perm_set_timing(1)  # CUDA events around each walk kernel (roofline)
     n = args.n
     a = W.c5(n)
     k0, k1 = shard_range("glynn", n, n, rank, world)

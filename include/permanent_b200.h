@@ -55,6 +55,9 @@ int perm_device_sm_count(void);
  * the last Gray-walk kernel launched by this host thread (-1 if none), and
  * its launch plan (grid size, log2 of the per-lane chunk length). */
 double perm_last_kernel_ms(void);
+/* Enable (1) / disable (0) the CUDA-event bracketing of walk kernels read by
+ * perm_last_kernel_ms (off by default: two event records per call). */
+int perm_set_timing(int on);
 int perm_last_kernel_plan(int* grid, int* log2L);
 /* FP64-pipe roofline denominator: DFMA/s sustained by an 8-chain DFMA
  * kernel over the whole device for about `seconds`. */

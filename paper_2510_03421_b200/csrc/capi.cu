@@ -126,6 +126,7 @@ int walk_partial(int alg, bool cplx, int m, int n, const double* a, int64_t lda,
                                   : reinterpret_cast<double*>(static_cast<char*>(s->dev) + s->dev_cap) - 8;
   st = run_walk(ws, k_begin, k_end, mag, dst, stream);
   if (st) return st;
+  if (partial_on_device) s->async_pending = true;
   if (!partial_on_device) {
     PERM_CUDA_TRY(cudaMemcpyAsync(s->host, dst, 8 * sizeof(double), cudaMemcpyDeviceToHost, stream));
     PERM_CUDA_TRY(cudaStreamSynchronize(stream));
@@ -181,6 +182,11 @@ double perm_last_kernel_ms(void) {
   float ms = 0.0f;
   if (cudaEventElapsedTime(&ms, t.start, t.stop) != cudaSuccess) return -1.0;
   return (double)ms;
+}
+
+int perm_set_timing(int on) {
+  set_timing(on != 0);
+  return PERM_OK;
 }
 
 int perm_last_kernel_plan(int* grid, int* log2L) {

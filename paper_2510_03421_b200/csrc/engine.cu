@@ -1,6 +1,7 @@
 // Host-side engine internals: error state, scratch, matrix staging, walk
 // setup/normalization and the fixed-order finalize kernel.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 
 #include "engine.cuh"
@@ -28,6 +29,8 @@ Scratch* scratch() {
   if (s->device != dev) {
     s->device = dev;
     if (cudaMallocHost(&s->host, kHostResultDoubles * sizeof(double)) != cudaSuccess) return nullptr;
+    if (cudaMalloc(&s->done, sizeof(unsigned int)) != cudaSuccess) return nullptr;
+    if (cudaMemset(s->done, 0, sizeof(unsigned int)) != cudaSuccess) return nullptr;
     // keep stream-ordered allocations cached across synchronizations (the
     // default release threshold of 0 returns them to the driver at every
     // sync, which made each batch call pay ~2 ms of re-mapping)
@@ -64,8 +67,11 @@ int stage_h2d(Scratch* s, void* dst, const void* src, size_t bytes, cudaStream_t
     s->stage_cap = cap;
   }
   // the staging buffer (and the scratch it feeds) may still be in use by an
-  // asynchronous call queued earlier on this stream
-  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  // asynchronous call (device-side partial) queued earlier on this thread
+  if (s->async_pending) {
+    PERM_CUDA_TRY(cudaDeviceSynchronize());
+    s->async_pending = false;
+  }
   std::memcpy(s->stage, src, bytes);
   PERM_CUDA_TRY(cudaMemcpyAsync(dst, s->stage, bytes, cudaMemcpyHostToDevice, stream));
   return PERM_OK;
@@ -221,6 +227,9 @@ void normalize(int alg, int m, int n, int scale_log2, double* re, double* im, do
 }
 
 // ---------------------------------------------------------------- timing
+static std::atomic<bool> g_timing{false};
+bool timing_enabled() { return g_timing.load(std::memory_order_relaxed); }
+void set_timing(bool on) { g_timing.store(on, std::memory_order_relaxed); }
 // CUDA events bracketing the last walk kernel launched by this host thread
 // (bench.py reads its duration for the live roofline figure).
 static thread_local KernelTimer g_timer[16];
@@ -283,32 +292,6 @@ int fp64_peak_probe(double seconds, double* dfma_per_s) {
 }
 
 // ---------------------------------------------------------------- kernels
-__global__ void walk_finalize_kernel(const double* __restrict__ partials, int nparts, double* __restrict__ out) {
-  __shared__ double red[256][5];
-  const int tid = threadIdx.x;
-  double h = 0, l = 0, h2 = 0, l2 = 0, mg = 0;
-  for (int i = tid; i < nparts; i += blockDim.x) {
-    const double* p = partials + (size_t)i * kPartialStride;
-    dd_add(h, l, p[0], p[1]);
-    dd_add(h2, l2, p[2], p[3]);
-    mg += p[4];
-  }
-  red[tid][0] = h; red[tid][1] = l; red[tid][2] = h2; red[tid][3] = l2; red[tid][4] = mg;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (tid < s) {
-      dd_add(red[tid][0], red[tid][1], red[tid + s][0], red[tid + s][1]);
-      dd_add(red[tid][2], red[tid][3], red[tid + s][2], red[tid + s][3]);
-      red[tid][4] += red[tid + s][4];
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    out[0] = red[0][0]; out[1] = red[0][1]; out[2] = red[0][2]; out[3] = red[0][3]; out[4] = red[0][4];
-    out[5] = 0.0; out[6] = 0.0; out[7] = 0.0;
-  }
-}
-
 walk_fn walk_lookup_f64_w0(int P);
 walk_fn walk_lookup_f64_w1(int P);
 walk_fn walk_lookup_c128_w0(int P);
@@ -355,16 +338,17 @@ int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, dou
   job.k_begin = k_begin;
   job.k_end = k_end;
   job.partials = partials;
+  job.final_out = dst;
+  job.done = s->done;
   WalkPlan plan;
   KernelTimer& tm = kernel_timer();
-  if (tm.ok) cudaEventRecord(tm.start, stream);
+  const bool timed = tm.ok && timing_enabled();
+  if (timed) cudaEventRecord(tm.start, stream);
   PERM_CUDA_TRY(fn(job, &plan, stream));
-  if (tm.ok) cudaEventRecord(tm.stop, stream);
-  tm.pending = tm.ok;
+  if (timed) cudaEventRecord(tm.stop, stream);
+  tm.pending = timed;
   tm.last_grid = plan.grid;
   tm.last_log2L = plan.log2L;
-  walk_finalize_kernel<<<1, 256, 0, stream>>>(partials, plan.grid, dst);
-  PERM_CUDA_TRY(cudaGetLastError());
   return PERM_OK;
 }
 

@@ -33,6 +33,8 @@ struct Scratch {
   double* host = nullptr;    // pinned host result buffer (kHostResultDoubles)
   void* stage = nullptr;     // pinned host staging buffer for H2D copies
   size_t stage_cap = 0;
+  unsigned int* done = nullptr;  // walk kernels' last-block counter (device)
+  bool async_pending = false;    // a device-output call may still be running
   cudaStream_t own = nullptr;
 };
 constexpr size_t kHostResultDoubles = 16384;    // pinned result buffer size
@@ -81,6 +83,8 @@ struct KernelTimer {
   int last_grid = 0, last_log2L = 0;
 };
 KernelTimer& kernel_timer();
+bool timing_enabled();
+void set_timing(bool on);
 int fp64_peak_probe(double seconds, double* dfma_per_s);
 
 }  // namespace permb200

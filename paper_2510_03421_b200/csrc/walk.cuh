@@ -27,8 +27,8 @@
 //
 // Accumulation: a plain FP64 sum over each chunk (<= L terms), folded into a
 // per-thread double-double with two_sum; double-double warp-shuffle and block
-// reductions; one partial (hi, lo) per block, combined in fixed order by
-// walk_finalize_kernel -> deterministic for a given launch shape.
+// reductions; one partial (hi, lo) per block, combined in fixed block order
+// by the last block to finish -> deterministic for a given launch shape.
 #pragma once
 #include "common.cuh"
 
@@ -49,7 +49,54 @@ struct WalkArgs {
   uint64_t k_begin;      // first Gray index, multiple of 32*L
   uint64_t ngroups;      // number of 32-chunk groups
   double* partials;      // [gridDim.x][kPartialStride]
+  double* final_out;     // 8 doubles: fixed-order sum of all block partials
+  unsigned int* done;    // block-completion counter (0 on entry, reset on exit)
 };
+
+// Last-block-done combine: every block publishes its partial, the block that
+// arrives last sums all partials in block order (deterministic for a given
+// grid) and writes the final 8 doubles -- no separate finalize launch.
+__device__ __forceinline__ void walk_last_block_combine(const double* partials, double* final_out,
+                                                        unsigned int* done) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = (atomicAdd(done, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int tid = threadIdx.x;
+  double h = 0, l = 0, h2 = 0, l2 = 0, mg = 0;
+  for (int i = tid; i < (int)gridDim.x; i += blockDim.x) {
+    const volatile double* p = partials + (size_t)i * kPartialStride;
+    dd_add(h, l, p[0], p[1]);
+    dd_add(h2, l2, p[2], p[3]);
+    mg += p[4];
+  }
+  __shared__ double red[32][5];
+  // fixed-order tree over the block: shuffles then warp leaders
+  for (int off = 16; off > 0; off >>= 1) {
+    dd_add(h, l, __shfl_down_sync(0xffffffffu, h, off), __shfl_down_sync(0xffffffffu, l, off));
+    dd_add(h2, l2, __shfl_down_sync(0xffffffffu, h2, off), __shfl_down_sync(0xffffffffu, l2, off));
+    mg += __shfl_down_sync(0xffffffffu, mg, off);
+  }
+  if ((tid & 31) == 0) {
+    red[tid >> 5][0] = h; red[tid >> 5][1] = l; red[tid >> 5][2] = h2; red[tid >> 5][3] = l2; red[tid >> 5][4] = mg;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double H = red[0][0], Lo = red[0][1], H2 = red[0][2], L2 = red[0][3], M = red[0][4];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      dd_add(H, Lo, red[w][0], red[w][1]);
+      dd_add(H2, L2, red[w][2], red[w][3]);
+      M += red[w][4];
+    }
+    final_out[0] = H; final_out[1] = Lo; final_out[2] = H2; final_out[3] = L2; final_out[4] = M;
+    final_out[5] = 0.0; final_out[6] = 0.0; final_out[7] = 0.0;
+    *done = 0u;  // ready for the next launch on this scratch
+  }
+}
 
 // Shared-memory reads of U rows go through `asm volatile` 128-bit loads on
 // purpose: with plain loads NVVM hoists every row read of the 8 unrolled
@@ -462,6 +509,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_ke
     double* out = args.partials + (size_t)blockIdx.x * kPartialStride;
     out[0] = H; out[1] = Lo; out[2] = Hi2; out[3] = Lo2; out[4] = M;
   }
+  walk_last_block_combine(args.partials, args.final_out, args.done);
 }
 
 // Single-thread walk for tiny index spaces (< 32 chunks of 8): runtime P.
@@ -499,10 +547,8 @@ __global__ void walk_small_kernel(const T* __restrict__ v0, const T* __restrict_
   }
   partials[0] = Num<T>::re(acc); partials[1] = 0.0;
   partials[2] = Num<T>::im(acc); partials[3] = 0.0;
-  partials[4] = mag;
+  partials[4] = mag; partials[5] = 0.0; partials[6] = 0.0; partials[7] = 0.0;
 }
 
-// Fixed-order combine of block partials -> out[0..4] (one block).
-__global__ void walk_finalize_kernel(const double* __restrict__ partials, int nparts, double* __restrict__ out);
 
 }  // namespace permb200

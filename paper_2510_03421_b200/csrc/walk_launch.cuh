@@ -18,6 +18,8 @@ struct WalkJob {
   uint64_t k_begin, k_end;  // Gray range; k_begin, k_end multiples of 32*L (or tiny range)
   int force_log2L = 0;       // tuning / test knob: chunk length exponent (0 = cost model)
   double* partials;      // device scratch, >= max_partials() * kPartialStride doubles
+  double* final_out;     // device, 8 doubles (combined result)
+  unsigned int* done;    // device counter, zero on entry
 };
 
 struct WalkPlan {
@@ -88,7 +90,7 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
     plan->grid = 1;
     plan->log2L = 0;
     walk_small_kernel<T, P><<<1, 32, 0, stream>>>(static_cast<const T*>(job.v0), static_cast<const T*>(job.U), job.w,
-                                               P, job.B, W ? 1 : 0, job.mag, job.k_begin, job.k_end, job.partials);
+                                               P, job.B, W ? 1 : 0, job.mag, job.k_begin, job.k_end, job.final_out);
     return cudaGetLastError();
   }
   WalkArgs a;
@@ -96,6 +98,8 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
   a.k_begin = job.k_begin;
   a.ngroups = (steps >> r) / 32;
   a.partials = job.partials;
+  a.final_out = job.final_out;
+  a.done = job.done;
   uint64_t grid = (uint64_t)bps * nsm;
   const uint64_t need = (a.ngroups + kWalkWarps - 1) / kWalkWarps;
   if (grid > need) grid = need;

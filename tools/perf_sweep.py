@@ -41,6 +41,7 @@ def kernel_ms():
 
 def main(out):
     lib = _lib.load()
+    lib.perm_set_timing(1)
     pk = _lib.out_buf(1)
     _lib.check(lib.perm_fp64_peak_probe(0.5, pk), "probe")
     peak = float(pk[0])
