@@ -141,6 +141,33 @@ int perm_walk_finish_f64(int alg, int m, int n, const double* a, int64_t lda, co
 int perm_walk_finish_c128(int alg, int m, int n, const double* a, int64_t lda, const double* partials, int G,
                           double* out, double* magsum);
 
+/* Exact integer shards.  width 64: the checked-int64 walk of one range,
+ * summarized as (sum, min/max running prefix, overflow flag) so that
+ * perm_walk_finish_i64 reproduces the reference's overflow flag exactly
+ * across shards (combined in rank order); not available for rectangular
+ * Ryser, whose checked kernel follows the lexicographic combination order
+ * (src/_kernels.py:265-365).  width 128: the range's walk sum mod 2^128
+ * plus its FP64 estimate and magnitude sum; the finish certifies the total
+ * fits and checks it against the summed estimate.  partial = 8 int64
+ * (opaque, tagged with the width).  finish: out[0..1] = lo/hi, as
+ * perm_glynn_i64. */
+int perm_walk_partial_i64(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width,
+                          uint64_t k_begin, uint64_t k_end, int64_t* partial, void* stream);
+int perm_walk_finish_i64(int alg, int m, int n, const int64_t* a, int64_t lda, int width, const int64_t* partials,
+                         int G, int64_t* out, int* fits_int64);
+
+/* ---- single-process multi-device driver (SURVEY 8(b) perm_sharded_*) -----
+ * One permanent over `ngpu` devices from one host process: shard i (of
+ * perm_walk_shard(i, ngpu)) runs on devices[i] from a persistent host worker,
+ * the caller combines in shard order.  `a` is host memory.  A device may be
+ * listed more than once (its shards then share it).  Synchronous. */
+int perm_sharded_f64(int alg, int m, int n, const double* a, int64_t lda, int ngpu, const int* devices, double* out,
+                     double* magsum);
+int perm_sharded_c128(int alg, int m, int n, const double* a, int64_t lda, int ngpu, const int* devices,
+                      double* out, double* magsum);
+int perm_sharded_i64(int alg, int m, int n, const int64_t* a, int64_t lda, int width, int ngpu, const int* devices,
+                     int64_t* out, int* fits_int64);
+
 /* ---- double-double validation walks -------------
  * Glynn or Ryser with double-double state, products and sums (~1e-30 unit
  * roundoff): the GPU cross-check where the reference cannot run and FP64

@@ -59,6 +59,16 @@ SIGNATURES = {
                                          C.c_uint64, C.c_int, _vp, C.c_int, _vp]),
     "perm_walk_finish_f64": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, _vp, C.c_int, _dp, _dp]),
     "perm_walk_finish_c128": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, _vp, C.c_int, _dp, _dp]),
+    "perm_walk_partial_i64": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, C.c_uint64,
+                                        C.c_uint64, _ip, _vp]),
+    "perm_walk_finish_i64": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _ip, C.c_int, _ip,
+                                       C.POINTER(C.c_int)]),
+    "perm_sharded_f64": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.POINTER(C.c_int), _dp,
+                                   _dp]),
+    "perm_sharded_c128": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.POINTER(C.c_int), _dp,
+                                    _dp]),
+    "perm_sharded_i64": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_int,
+                                   C.POINTER(C.c_int), _ip, C.POINTER(C.c_int)]),
     "perm_select": (C.c_int, [C.c_int, C.c_int, _dp, C.c_int64, C.c_int]),
 }
 

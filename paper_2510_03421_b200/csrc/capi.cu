@@ -1,6 +1,10 @@
 // extern "C" entry points of libpermanent_b200.so (include/permanent_b200.h).
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 
 #include "engine.cuh"
 
@@ -17,6 +21,10 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
 int batch_select(int m, int n);
 int dd_permanent(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out4,
                  void* stream);
+int int_walk_partial(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, uint64_t k0,
+                     uint64_t k1, int64_t* partial, void* stream);
+int int_walk_finish(int alg, int m, int n, const int64_t* a, int64_t lda, int width, const int64_t* partials, int G,
+                    int64_t* out, int* fits_int64);
 }
 
 namespace {
@@ -160,6 +168,121 @@ int walk_finish(int alg, bool cplx, int m, int n, const double* a, int64_t lda, 
   if (cplx) out[1] = im;
   if (magsum) *magsum = mg;
   return PERM_OK;
+}
+
+// ---- single-process multi-device driver (perm_sharded_*) ------------------
+// One persistent host worker per shard slot: slot i binds devices[i] and
+// walks shard i of `ngpu` with the single-device code path (its own
+// thread-local scratch and the per-thread default stream of that device);
+// the caller's thread combines the partials in shard order.  The exchange is
+// 64 bytes per device once per permanent, so it goes through pinned host
+// memory; nothing on the data path is collective.
+class ShardPool {
+ public:
+  // run fns[i] on worker i, wait for all
+  void run(const std::vector<std::function<void()>>& fns) {
+    std::unique_lock<std::mutex> call(call_mu_);  // one sharded call at a time
+    while (workers_.size() < fns.size()) workers_.emplace_back(new Worker());
+    for (size_t i = 0; i < fns.size(); ++i) workers_[i]->post(fns[i]);
+    for (size_t i = 0; i < fns.size(); ++i) workers_[i]->wait();
+  }
+
+ private:
+  struct Worker {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::function<void()> job;
+    bool busy = false;
+    Worker() {
+      std::thread([this] {
+        for (;;) {
+          std::function<void()> f;
+          {
+            std::unique_lock<std::mutex> lk(mu);
+            cv.wait(lk, [this] { return (bool)job; });
+            f = std::move(job);
+          }
+          f();
+          {
+            std::lock_guard<std::mutex> lk(mu);
+            busy = false;
+          }
+          cv.notify_all();
+        }
+      }).detach();  // workers live for the process (their scratch is thread-local)
+    }
+    void post(std::function<void()> f) {
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        busy = true;
+        job = std::move(f);
+      }
+      cv.notify_all();
+    }
+    void wait() {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [this] { return !busy; });
+    }
+  };
+  std::mutex call_mu_;
+  std::vector<Worker*> workers_;  // never freed: detached threads reference them
+};
+
+ShardPool& shard_pool() {
+  static ShardPool* p = new ShardPool();
+  return *p;
+}
+
+struct ShardStatus {
+  int st = PERM_OK;
+  std::string err;
+};
+
+// Run `body(i, k0, k1)` for every shard i on devices[i]; first failure wins.
+int run_shards(int alg, int m, int n, int ngpu, const int* devices,
+               const std::function<int(int, uint64_t, uint64_t)>& body) {
+  if (ngpu < 1 || ngpu > 64 || devices == nullptr) {
+    set_error("ngpu must be 1..64 with a device list");
+    return PERM_BAD_ARG;
+  }
+  std::vector<ShardStatus> res(ngpu);
+  std::vector<std::function<void()>> fns;
+  for (int i = 0; i < ngpu; ++i) {
+    fns.push_back([&, i] {
+      uint64_t k0 = 0, k1 = 0;
+      int st = perm_walk_shard(alg, m, n, i, ngpu, &k0, &k1);
+      if (!st) {
+        const cudaError_t e = cudaSetDevice(devices[i]);
+        st = e == cudaSuccess ? body(i, k0, k1) : cuda_fail(e, "cudaSetDevice");
+      }
+      res[i].st = st;
+      if (st) res[i].err = last_error();
+    });
+  }
+  shard_pool().run(fns);
+  for (int i = 0; i < ngpu; ++i)
+    if (res[i].st) {
+      set_error("shard " + std::to_string(i) + " (device " + std::to_string(devices[i]) + "): " + res[i].err);
+      return res[i].st;
+    }
+  return PERM_OK;
+}
+
+int sharded_float(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int ngpu, const int* devices,
+                  double* out, double* magsum) {
+  clear_error();
+  int st = check_shape(alg, m, n);
+  if (st) return st;
+  if (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER) {
+    set_error("sharded walks are Glynn or Ryser");
+    return PERM_BAD_ARG;
+  }
+  std::vector<double> parts((size_t)std::max(ngpu, 1) * 8, 0.0);
+  st = run_shards(alg, m, n, ngpu, devices, [&](int i, uint64_t k0, uint64_t k1) {
+    return walk_partial(alg, cplx, m, n, a, lda, 0, k0, k1, magsum != nullptr, &parts[(size_t)i * 8], 0, nullptr);
+  });
+  if (st) return st;
+  return walk_finish(alg, cplx, m, n, a, lda, parts.data(), ngpu, out, magsum);
 }
 
 }  // namespace
@@ -315,6 +438,36 @@ int perm_walk_finish_f64(int alg, int m, int n, const double* a, int64_t lda, co
 int perm_walk_finish_c128(int alg, int m, int n, const double* a, int64_t lda, const double* partials, int G,
                           double* out, double* magsum) {
   return walk_finish(alg, true, m, n, a, lda, partials, G, out, magsum);
+}
+
+int perm_walk_partial_i64(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width,
+                          uint64_t k_begin, uint64_t k_end, int64_t* partial, void* stream) {
+  return int_walk_partial(alg, m, n, a, lda, dev_ptr, width, k_begin, k_end, partial, stream);
+}
+int perm_walk_finish_i64(int alg, int m, int n, const int64_t* a, int64_t lda, int width, const int64_t* partials,
+                         int G, int64_t* out, int* fits_int64) {
+  return int_walk_finish(alg, m, n, a, lda, width, partials, G, out, fits_int64);
+}
+
+int perm_sharded_f64(int alg, int m, int n, const double* a, int64_t lda, int ngpu, const int* devices, double* out,
+                     double* magsum) {
+  return sharded_float(alg, false, m, n, a, lda, ngpu, devices, out, magsum);
+}
+int perm_sharded_c128(int alg, int m, int n, const double* a, int64_t lda, int ngpu, const int* devices,
+                      double* out, double* magsum) {
+  return sharded_float(alg, true, m, n, a, lda, ngpu, devices, out, magsum);
+}
+int perm_sharded_i64(int alg, int m, int n, const int64_t* a, int64_t lda, int width, int ngpu, const int* devices,
+                     int64_t* out, int* fits_int64) {
+  clear_error();
+  int st = check_shape(alg, m, n);
+  if (st) return st;
+  std::vector<int64_t> parts((size_t)std::max(ngpu, 1) * 8, 0);
+  st = run_shards(alg, m, n, ngpu, devices, [&](int i, uint64_t k0, uint64_t k1) {
+    return int_walk_partial(alg, m, n, a, lda, 0, width, k0, k1, &parts[(size_t)i * 8], nullptr);
+  });
+  if (st) return st;
+  return int_walk_finish(alg, m, n, a, lda, width, parts.data(), ngpu, out, fits_int64);
 }
 
 // src/dispatch.py:84-95 (strict '>' comparisons: ties take the else branch)

@@ -132,15 +132,40 @@ struct DevBuf {
   }
 };
 
+// ------------------------------------------------------------ Gray ranges
+// Every integer walk below runs over one Gray range [k0, k1) (the whole walk
+// for a single call, one shard for a sharded one).  Chunks of 2^log2L must
+// tile the range, so log2L is capped by the alignment of k0 and k1 - k0.
+static int range_align(uint64_t k0, uint64_t k1) {
+  const uint64_t len = k1 - k0;
+  int a = len ? __builtin_ctzll(len) : 0;
+  if (k0) a = std::min(a, __builtin_ctzll(k0));
+  return a;
+}
+
+// One Gray range's contribution to an exact integer permanent; serialized
+// as 8 int64 by perm_walk_partial_i64.
+struct IntPart {
+  // CHECKED (width 64): ordered summary (sum, min/max running prefix) of the
+  // range's terms and the reference's overflow flag
+  s128 S = 0, mn = 0, mx = 0;
+  bool flag = false;
+  // WRAP (width 128): the range's sum mod 2^128, and an FP64 estimate of it
+  // (raw-sum units) with its magnitude sum for the fit certificate
+  unsigned __int128 raw = 0;
+  double est_hi = 0, est_lo = 0, mag = 0;
+  int est_kind = 0;  // 0 none, 1 fused FP64-exact walk, 2 separate float walk
+  bool refused = false;  // entries too large for the FP64 certificate
+};
+
 // ------------------------------------------------------------ CHECKED walk
-// Returns PERM_OK with *ovf and *value (the raw walk sum when !ovf).
-static int checked_walk(const IntSetup& s, cudaStream_t stream, bool* ovf, int64_t* value) {
-  *ovf = s.pre_overflow;
-  *value = 0;
-  if (*ovf) return PERM_OK;
-  const uint64_t steps = 1ull << s.B;
+static int checked_range(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream_t stream, IntPart* p) {
+  p->flag = s.pre_overflow;
+  if (p->flag || k1 == k0) return PERM_OK;
+  const uint64_t steps = k1 - k0;
+  const int amax = range_align(k0, k1);
   int log2L = 0;
-  while ((steps >> log2L) > (1ull << 17)) ++log2L;
+  while (log2L < amax && (steps >> log2L) > (1ull << 17)) ++log2L;
   const uint64_t nchunks = steps >> log2L;
   const uint64_t blocks = (nchunks + kIntThreads - 1) / kIntThreads;
   const size_t nv0 = s.v0.size(), nU = s.U.size();
@@ -158,7 +183,7 @@ static int checked_walk(const IntSetup& s, cudaStream_t stream, bool* ovf, int64
   a.B = s.B;
   a.log2L = log2L;
   a.wlen = 0;
-  a.k_begin = 0;
+  a.k_begin = k0;
   a.nchunks = nchunks;
   a.out = d + nv0 + nU;
   int_walk_checked_kernel<<<(unsigned)blocks, kIntThreads, 0, stream>>>(a);
@@ -168,19 +193,20 @@ static int checked_walk(const IntSetup& s, cudaStream_t stream, bool* ovf, int64
   PERM_CUDA_TRY(cudaStreamSynchronize(stream));
   PERM_CUDA_TRY(cudaFreeAsync(buf.p, stream));
   buf.p = nullptr;
-  // ordered combine of block summaries (Gray order = block order)
-  s128 G = 0;
-  bool flag = false;
+  // ordered combine of block summaries (Gray order = block order); the
+  // empty prefix (0) is included, as in the kernel's identity element
+  s128 G = 0, mn = 0, mx = 0;
   for (uint64_t b = 0; b < blocks; ++b) {
     const int64_t* o = &h[b * 8];
     auto get = [&](int q) { return (s128)(((unsigned __int128)(uint64_t)o[q + 1] << 64) | (uint64_t)o[q]); };
-    if (o[6]) flag = true;
-    s128 S = get(0), mn = get(2), mx = get(4);
-    if (G + mn < kI64Min || G + mx > kI64Max) flag = true;
-    G += S;
+    if (o[6]) p->flag = true;
+    mn = std::min(mn, G + get(2));
+    mx = std::max(mx, G + get(4));
+    G += get(0);
   }
-  *ovf = flag;
-  *value = flag ? 0 : (int64_t)G;
+  p->S = G;
+  p->mn = mn;
+  p->mx = mx;
   return PERM_OK;
 }
 
@@ -190,18 +216,20 @@ walk_fn_if int_wrap_fp_lookup(int P);
 
 // Fused path: FP64-exact state and group products (|state| <= 83), the
 // int128 sum and its FP64 estimate / magnitude sum from one kernel.
-static bool fp_walk_ok(const IntSetup& s) {
-  return !s.weighted && s.bound <= 83 && s.B >= 8 && s.P >= 1 && s.P <= 64;
+static bool fp_walk_ok(const IntSetup& s, uint64_t k0, uint64_t k1) {
+  return !s.weighted && s.bound <= 83 && s.B >= 8 && s.P >= 1 && s.P <= 64 && k1 - k0 >= 8 &&
+         range_align(k0, k1) >= 3;
 }
 
-static int wrap_walk_fp(const IntSetup& s, cudaStream_t stream, s128* raw, long double* est, long double* mag) {
-  const uint64_t steps = 1ull << s.B;
+static int wrap_range_fp(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream_t stream, IntPart* p) {
+  const uint64_t steps = k1 - k0;
+  const int amax = range_align(k0, k1);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t lanes = (uint64_t)nsm * 8 * kIntThreads;
   int log2L = 3;
-  while (log2L < 14 && (steps >> (log2L + 1)) >= 16 * lanes) ++log2L;
+  while (log2L < 14 && log2L < amax && (steps >> (log2L + 1)) >= 16 * lanes) ++log2L;
   const uint64_t nchunks = steps >> log2L;
   const uint64_t blocks = std::min<uint64_t>((nchunks + kIntThreads - 1) / kIntThreads, (uint64_t)nsm * 8);
   std::vector<double> buf(s.v0.size() + s.U.size());
@@ -218,7 +246,7 @@ static int wrap_walk_fp(const IntSetup& s, cudaStream_t stream, s128* raw, long 
   a.P = s.P;
   a.B = s.B;
   a.log2L = log2L;
-  a.k_begin = 0;
+  a.k_begin = k0;
   a.nchunks = nchunks;
   a.out = reinterpret_cast<int64_t*>(d + buf.size());
   walk_fn_if fn = int_wrap_fp_lookup(s.P);
@@ -244,26 +272,28 @@ static int wrap_walk_fp(const IntSetup& s, cudaStream_t stream, s128* raw, long 
     dd_add(H, L, hh, ll);
     M += mm;
   }
-  *raw = (s128)acc;
-  *est = (long double)H + (long double)L;
-  *mag = M;
+  p->raw = acc;
+  p->est_hi = H;
+  p->est_lo = L;
+  p->mag = M;
+  p->est_kind = 1;
   return PERM_OK;
 }
 
-static int wrap_walk(const IntSetup& s, cudaStream_t stream, s128* raw) {
+static int wrap_range(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream_t stream, IntPart* p) {
+  if (k1 == k0) return PERM_OK;
   const bool wide = s.bound >= ((s128)1 << 62);  // int64 state could wrap
-  const uint64_t steps = 1ull << s.B;
+  const uint64_t steps = k1 - k0;
+  const int amax = range_align(k0, k1);
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   // exact int64 groups of 8 factors need bound^8 < 2^63
   const bool g8 = !wide && !s.weighted && (long double)s.bound < std::pow(2.0L, 63.0L / 8.0L) && steps >= 8;
   const uint64_t lanes = (uint64_t)nsm * 8 * kIntThreads;
-  int log2L = 3;
-  while (log2L < 14 && (steps >> (log2L + 1)) >= 16 * lanes) ++log2L;
-  while (log2L > 0 && (steps >> log2L) < 1) --log2L;
+  int log2L = std::min(3, amax);
+  while (log2L < 14 && log2L < amax && (steps >> (log2L + 1)) >= 16 * lanes) ++log2L;
   if (!g8 && log2L > 10) log2L = 10;
-  if (steps < 8) log2L = 0;
   const uint64_t nchunks = steps >> log2L;
   uint64_t blocks = std::min<uint64_t>((nchunks + kIntThreads - 1) / kIntThreads, (uint64_t)nsm * 8);
   const size_t nv0 = wide ? s.v0w.size() : s.v0.size(), nU = s.U.size(), nw = s.w.size();
@@ -282,7 +312,7 @@ static int wrap_walk(const IntSetup& s, cudaStream_t stream, s128* raw) {
   a.B = s.B;
   a.log2L = log2L;
   a.wlen = (int)nw;
-  a.k_begin = 0;
+  a.k_begin = k0;
   a.nchunks = nchunks;
   a.out = d + nv0 + nU + nw;
   walk_fn_i fast = (g8 && log2L >= 3) ? int_wrap_lookup(s.P) : nullptr;
@@ -303,15 +333,18 @@ static int wrap_walk(const IntSetup& s, cudaStream_t stream, s128* raw) {
   unsigned __int128 acc = 0;
   for (uint64_t b = 0; b < blocks; ++b)
     acc += ((unsigned __int128)(uint64_t)h[2 * b + 1] << 64) | (uint64_t)h[2 * b];
-  *raw = (s128)acc;
+  p->raw = acc;
   return PERM_OK;
 }
 
-// Float estimate for the int128 fit certificate: same algorithm in FP64
-// with the magnitude sum M; |per - per_fp| <= (P + 2^14 + 16) * 2^-52 * M
-// (exact integer state entries; <= P-1 product roundings; chunk sums of at
-// most 2^14 terms; double-double above that).
-static int float_estimate(int alg, const IntMat& A, cudaStream_t stream, double* per, double* mag) {
+// FP64 estimate of a range's raw sum for the fit certificate: the float walk
+// with the magnitude sum M.  |raw - est| <= (P + 2^14 + 16) u M (exact state
+// entries, <= P-1 product roundings, chunk sums of <= 2^14 terms, double-
+// double above).  Rectangular Glynn walks the pre-scaled matrix 2^s A, whose
+// raw sum is 2^(s m) times the integer walk's: undone exactly.
+static int float_range(int alg, const IntMat& A, uint64_t k0, uint64_t k1, cudaStream_t stream, IntPart* p) {
+  p->est_kind = 2;
+  if (k1 == k0) return PERM_OK;
   HostMat H;
   H.m = A.m;
   H.n = A.n;
@@ -327,21 +360,78 @@ static int float_estimate(int alg, const IntMat& A, cudaStream_t stream, double*
   st = ensure_dev(sc, part_bytes + ws.buf.size() * sizeof(double) + 64 * sizeof(double) + 256);
   if (st) return st;
   double* dst = reinterpret_cast<double*>(static_cast<char*>(sc->dev) + sc->dev_cap) - 8;
-  st = run_walk(ws, 0, walk_steps(alg, A.m, A.n), 1, dst, stream);
+  st = run_walk(ws, k0, k1, 1, dst, stream);
   if (st) return st;
   PERM_CUDA_TRY(cudaMemcpyAsync(sc->host, dst, 8 * sizeof(double), cudaMemcpyDeviceToHost, stream));
   PERM_CUDA_TRY(cudaStreamSynchronize(stream));
-  double re = sc->host[0] + sc->host[1], im = 0.0, mg = sc->host[4];
-  normalize(alg, A.m, A.n, ws.scale_log2, &re, &im, &mg);
-  *per = re;
-  *mag = mg;
+  const int e = -ws.scale_log2 * A.m;
+  p->est_hi = std::ldexp(sc->host[0], e);
+  p->est_lo = std::ldexp(sc->host[1], e);
+  p->mag = std::ldexp(sc->host[4], e);
   return PERM_OK;
 }
 
-static bool fits_bound(double per_fp, double mag, int P, long double denom) {
-  const long double E = (long double)(P + (1 << 14) + 16) * std::ldexp(1.0L, -52) * (long double)mag;
-  const long double hi = ((long double)std::fabs(per_fp) + E) * denom;
-  return hi < std::ldexp(1.0L, 126);  // one bit of margin below 2^127
+// ------------------------------------------------------------ certificate
+struct IntPlan {
+  IntMat A;
+  IntSetup s;
+  s128 denom = 1;           // Glynn: 2^(n-1) (n-m)!
+  bool cert_apriori = false;  // |raw| < 2^126 from row/column sums alone
+};
+
+static int plan_int(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, cudaStream_t stream,
+                    IntPlan* pl) {
+  int st = load_int_matrix(m, n, a, lda, dev_ptr, &pl->A, stream);
+  if (st) return st;
+  setup_int(alg, pl->A, &pl->s);
+  pl->denom = 1;
+  if (alg == PERM_ALG_GLYNN) {
+    pl->denom = (s128)1 << (n - 1);
+    for (int i = 2; i <= n - m; ++i) pl->denom *= i;
+  }
+  // |raw| = |per| * denom <= per(|A|) * denom, and per(|A|) is at most the
+  // product of the row sums of |A| (and, square, of the column sums)
+  long double rows = 1.0L, cols = 1.0L;
+  for (int i = 0; i < m; ++i) {
+    long double r = 0;
+    for (int j = 0; j < n; ++j) r += std::fabs((long double)pl->A.at(i, j));
+    rows *= r;
+  }
+  for (int j = 0; j < n; ++j) {
+    long double c = 0;
+    for (int i = 0; i < m; ++i) c += std::fabs((long double)pl->A.at(i, j));
+    cols *= c;
+  }
+  const long double apriori = (m == n ? std::min(rows, cols) : rows) * (long double)pl->denom;
+  pl->cert_apriori = apriori < std::ldexp(1.0L, 126);
+  return PERM_OK;
+}
+
+static long double est_error(const IntPart& p, int P) {
+  const long double c = p.est_kind == 1 ? (3 + (1 << 14) + 16) : (P + (1 << 14) + 16);
+  return c * std::ldexp(1.0L, -52) * (long double)p.mag;
+}
+
+// One range.  `full` (the whole walk on one device) lets the separate float
+// estimate refuse before the exact walk is spent.
+static int int_part(int alg, const IntPlan& pl, int width, uint64_t k0, uint64_t k1, bool full, cudaStream_t stream,
+                    IntPart* p) {
+  const IntSetup& s = pl.s;
+  if (width == 64) return checked_range(s, k0, k1, stream, p);
+  if (fp_walk_ok(s, k0, k1)) return wrap_range_fp(s, k0, k1, stream, p);
+  if (!pl.cert_apriori) {
+    if (s.bound >= ((s128)1 << 52)) {  // state entries not exact in FP64
+      p->refused = true;
+      return PERM_OK;
+    }
+    int st = float_range(alg, pl.A, k0, k1, stream, p);
+    if (st) return st;
+    if (full && (long double)std::fabs(p->est_hi) + est_error(*p, s.P) >= std::ldexp(1.0L, 126)) {
+      p->refused = true;
+      return PERM_OK;
+    }
+  }
+  return wrap_range(s, k0, k1, stream, p);
 }
 
 static int to_out(s128 v, int64_t* out, int* fits_int64) {
@@ -351,127 +441,200 @@ static int to_out(s128 v, int64_t* out, int* fits_int64) {
   return PERM_OK;
 }
 
-int int_permanent(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, int64_t* out,
-                  int* fits_int64, void* stream_) {
-  clear_error();
-  cudaStream_t stream = pick_stream(stream_);
-  IntMat A;
-  int st = load_int_matrix(m, n, a, lda, dev_ptr, &A, stream);
-  if (st) return st;
-  IntSetup s;
-  setup_int(alg, A, &s);
-  s128 denom = 1;
-  if (alg == PERM_ALG_GLYNN) {
-    denom = (s128)1 << (n - 1);
-    for (int i = 2; i <= n - m; ++i) denom *= i;
-  }
+// Combine the ranges' parts in Gray order and normalize.
+static int int_finish(int alg, const IntPlan& pl, int width, const IntPart* parts, int G, int64_t* out,
+                      int* fits_int64) {
+  const int m = pl.A.m, n = pl.A.n;
   if (width == 64) {
     // reference semantics: PERM_OVERFLOW whenever the reference flags
-    bool ovf = false;
-    int64_t raw = 0;
-    st = checked_walk(s, stream, &ovf, &raw);
-    if (st) return st;
-    if (ovf) {
+    s128 T = 0;
+    bool flag = false;
+    for (int g = 0; g < G && !flag; ++g) {
+      const IntPart& p = parts[g];
+      if (p.flag || T + p.mn < kI64Min || T + p.mx > kI64Max) flag = true;
+      T += p.S;
+    }
+    if (flag) {
       set_error("an int64 intermediate overflowed (reference semantics)");
       return PERM_OVERFLOW;
     }
-    s128 v = raw;
+    s128 v = (int64_t)T;
     if (alg == PERM_ALG_GLYNN) {
-      if (v % denom != 0) {  // src/algorithms.py:436-437, 459-460
+      if (v % pl.denom != 0) {  // src/algorithms.py:436-437, 459-460
         set_error("Glynn sum not divisible by its normalization");
         return PERM_OVERFLOW;
       }
-      v /= denom;
+      v /= pl.denom;
     } else if (m == n && (n & 1)) {
       v = (s128)(int64_t)(0 - (uint64_t)(int64_t)v);  // int64 negation as in src/_kernels.py:216-217
     }
     return to_out(v, out, fits_int64);
   }
-  if (width != 128) {
-    set_error("width must be 64 or 128");
-    return PERM_BAD_ARG;
-  }
-  // Fit certificate for |walk sum| < 2^127: (a) a priori, or (b) an FP64 run
-  // with its magnitude-sum error bound (state entries must then be exactly
-  // representable, i.e. magnitudes < 2^52).
-  // (a): |walk sum| = |per| * denom <= per(|A|) * denom, and per(|A|) is at most
-  // the product of the row sums of |A| (and, square, of the column sums)
-  long double rows = 1.0L, cols = 1.0L;
-  for (int i = 0; i < m; ++i) {
-    long double r = 0;
-    for (int j = 0; j < n; ++j) r += std::fabs((long double)A.at(i, j));
-    rows *= r;
-  }
-  for (int j = 0; j < n; ++j) {
-    long double c = 0;
-    for (int i = 0; i < m; ++i) c += std::fabs((long double)A.at(i, j));
-    cols *= c;
-  }
-  const long double apriori = (m == n ? std::min(rows, cols) : rows) * (long double)denom;
-  const bool cert_apriori = apriori < std::ldexp(1.0L, 126);
-  if (fp_walk_ok(s)) {
-    // one pass: exact int128 walk + its own FP64 estimate.  Error of the
-    // estimate of the raw sum: <= 3 product roundings per term (group
-    // products are exact) and chunk sums of <= 2^14 terms, i.e.
-    // E <= (3 + 2^14 + 16) u M_raw.
-    s128 raw = 0;
-    long double est = 0, mag_raw = 0;
-    st = wrap_walk_fp(s, stream, &raw, &est, &mag_raw);
-    if (st) return st;
-    const long double E = (long double)(3 + (1 << 14) + 16) * std::ldexp(1.0L, -52) * mag_raw;
-    if (!cert_apriori && std::fabs(est) + E >= std::ldexp(1.0L, 126)) {
-      set_error("exact value not certified to fit the int128 walk");
+  // width 128: sum mod 2^128; certify |raw| < 2^126 (a priori, or by the
+  // summed FP64 estimate and its error bound) and cross-check the estimate
+  unsigned __int128 acc = 0;
+  double H = 0, L = 0;
+  long double E = 0;
+  bool have_est = true;
+  for (int g = 0; g < G; ++g) {
+    const IntPart& p = parts[g];
+    if (p.refused) {
+      set_error(pl.s.bound >= ((s128)1 << 52)
+                    ? "exact value not certified to fit int128 (entries too large for the FP64 certificate)"
+                    : "exact value not certified to fit the int128 walk");
       return PERM_OVERFLOW;
     }
-    if (std::fabs((long double)raw - est) > E + 1.0L) {
-      set_error("internal: int128 walk disagrees with its FP64 estimate");
+    acc += p.raw;
+    if (p.est_kind == 0) {
+      have_est = false;
+    } else {
+      dd_add(H, L, p.est_hi, p.est_lo);
+      E += est_error(p, pl.s.P);
+    }
+  }
+  const long double est = (long double)H + (long double)L;
+  if (!pl.cert_apriori) {
+    if (!have_est) {
+      set_error("internal: no FP64 estimate for the int128 fit certificate");
       return PERM_CUDA;
     }
-    s128 v = raw;
-    if (alg == PERM_ALG_GLYNN) {
-      if (v % denom != 0) {
-        set_error("internal: Glynn int128 sum not divisible by its normalization");
-        return PERM_CUDA;
-      }
-      v /= denom;
-    } else if (m == n && (n & 1)) {
-      v = -v;
-    }
-    return to_out(v, out, fits_int64);
-  }
-  double per_fp = 0, mag = 0;
-  if (!cert_apriori) {
-    if (s.bound >= ((s128)1 << 52)) {
-      set_error("exact value not certified to fit int128 (entries too large for the FP64 certificate)");
-      return PERM_OVERFLOW;
-    }
-    st = float_estimate(alg, A, stream, &per_fp, &mag);
-    if (st) return st;
-    if (!fits_bound(per_fp, mag, s.P, (long double)denom)) {
+    if (std::fabs(est) + E >= std::ldexp(1.0L, 126)) {
       set_error("exact value not certified to fit the int128 walk");
       return PERM_OVERFLOW;
     }
   }
-  s128 raw = 0;
-  st = wrap_walk(s, stream, &raw);
-  if (st) return st;
+  const s128 raw = (s128)acc;
+  if (have_est && std::fabs((long double)raw - est) > E + 1.0L + std::ldexp(std::fabs(est), -60)) {
+    set_error("internal: int128 walk disagrees with its FP64 estimate");
+    return PERM_CUDA;
+  }
   s128 v = raw;
   if (alg == PERM_ALG_GLYNN) {
-    if (v % denom != 0) {
+    if (v % pl.denom != 0) {
       set_error("internal: Glynn int128 sum not divisible by its normalization");
       return PERM_CUDA;
     }
-    v /= denom;
+    v /= pl.denom;
   } else if (m == n && (n & 1)) {
     v = -v;
   }
-  // consistency with the FP64 estimate (catches a corrupted exact sum)
-  const long double E = (long double)(s.P + (1 << 14) + 16) * std::ldexp(1.0L, -52) * (long double)mag;
-  if (!cert_apriori && std::fabs((long double)v - (long double)per_fp) > E + 1.0L) {
-    set_error("internal: int128 result disagrees with the FP64 estimate");
-    return PERM_CUDA;
-  }
   return to_out(v, out, fits_int64);
+}
+
+int int_permanent(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, int64_t* out,
+                  int* fits_int64, void* stream_) {
+  clear_error();
+  if (width != 64 && width != 128) {
+    set_error("width must be 64 or 128");
+    return PERM_BAD_ARG;
+  }
+  cudaStream_t stream = pick_stream(stream_);
+  IntPlan pl;
+  int st = plan_int(alg, m, n, a, lda, dev_ptr, stream, &pl);
+  if (st) return st;
+  IntPart p;
+  st = int_part(alg, pl, width, 0, walk_steps(alg, m, n), true, stream, &p);
+  if (st) return st;
+  return int_finish(alg, pl, width, &p, 1, out, fits_int64);
+}
+
+// ------------------------------------------------------------ sharded
+static const int64_t kTag64 = 0x7065726d36340000LL, kTag128 = 0x7065726d31323800LL;
+
+static void put128(int64_t* o, s128 v) {
+  o[0] = (int64_t)(uint64_t)v;
+  o[1] = (int64_t)(uint64_t)((unsigned __int128)v >> 64);
+}
+static s128 get128(const int64_t* o) {
+  return (s128)(((unsigned __int128)(uint64_t)o[1] << 64) | (uint64_t)o[0]);
+}
+
+static int check_int_shardable(int alg, int m, int n, int width) {
+  if (width != 64 && width != 128) {
+    set_error("width must be 64 or 128");
+    return PERM_BAD_ARG;
+  }
+  if (width == 64 && alg == PERM_ALG_RYSER && m < n) {
+    set_error("checked rectangular Ryser replays the lexicographic combination order (not sharded); use width 128");
+    return PERM_BAD_ARG;
+  }
+  if (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER) {
+    set_error("sharded walks are Glynn or Ryser");
+    return PERM_BAD_ARG;
+  }
+  return PERM_OK;
+}
+
+int int_walk_partial(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, uint64_t k0,
+                     uint64_t k1, int64_t* partial, void* stream_) {
+  clear_error();
+  int st = check_int_shardable(alg, m, n, width);
+  if (st) return st;
+  cudaStream_t stream = pick_stream(stream_);
+  IntPlan pl;
+  st = plan_int(alg, m, n, a, lda, dev_ptr, stream, &pl);
+  if (st) return st;
+  if (k0 > k1 || k1 > walk_steps(alg, m, n)) {
+    set_error("Gray range outside the walk");
+    return PERM_BAD_ARG;
+  }
+  IntPart p;
+  st = int_part(alg, pl, width, k0, k1, false, stream, &p);
+  if (st) return st;
+  std::fill(partial, partial + 8, 0);
+  if (width == 64) {
+    put128(partial, p.S);
+    put128(partial + 2, p.mn);
+    put128(partial + 4, p.mx);
+    partial[6] = p.flag ? 1 : 0;
+    partial[7] = kTag64;
+  } else {
+    put128(partial, (s128)p.raw);
+    std::memcpy(&partial[2], &p.est_hi, 8);
+    std::memcpy(&partial[3], &p.est_lo, 8);
+    std::memcpy(&partial[4], &p.mag, 8);
+    partial[5] = p.est_kind;
+    partial[6] = p.refused ? 1 : 0;
+    partial[7] = kTag128;
+  }
+  return PERM_OK;
+}
+
+int int_walk_finish(int alg, int m, int n, const int64_t* a, int64_t lda, int width, const int64_t* partials, int G,
+                    int64_t* out, int* fits_int64) {
+  clear_error();
+  int st = check_int_shardable(alg, m, n, width);
+  if (st) return st;
+  if (G < 1) {
+    set_error("no partials");
+    return PERM_BAD_ARG;
+  }
+  IntPlan pl;
+  st = plan_int(alg, m, n, a, lda, 0, nullptr, &pl);
+  if (st) return st;
+  std::vector<IntPart> parts(G);
+  for (int g = 0; g < G; ++g) {
+    const int64_t* o = partials + 8 * (size_t)g;
+    IntPart& p = parts[g];
+    if (o[7] != (width == 64 ? kTag64 : kTag128)) {
+      set_error("partial was not produced by perm_walk_partial_i64 with this width");
+      return PERM_BAD_ARG;
+    }
+    if (width == 64) {
+      p.S = get128(o);
+      p.mn = get128(o + 2);
+      p.mx = get128(o + 4);
+      p.flag = o[6] != 0;
+    } else {
+      p.raw = (unsigned __int128)get128(o);
+      std::memcpy(&p.est_hi, &o[2], 8);
+      std::memcpy(&p.est_lo, &o[3], 8);
+      std::memcpy(&p.mag, &o[4], 8);
+      p.est_kind = (int)o[5];
+      p.refused = o[6] != 0;
+    }
+  }
+  return int_finish(alg, pl, width, parts.data(), G, out, fits_int64);
 }
 
 }  // namespace permb200

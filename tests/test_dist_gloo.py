@@ -36,6 +36,16 @@ def oracle_partial(alg, a, k0, k1):
     return [rh, rl, 0, 0, 0, 0, 0, 0]
 
 
+def oracle_int_partial(alg, a, k0, k1):
+    """Exact int128 range sum from the oracle, packed as the engine's
+    width-128 partial (the finish then uses the a-priori fit certificate)."""
+    sys.path.insert(0, str(ROOT))
+    from oracle import oracle as O
+    from paper_2510_03421_b200.sharded import int128_partial
+
+    return int128_partial(O.walk_i128_mt(O.walk_setup(alg, a), k0, k1, nthreads=1))
+
+
 def _worker(rank, world, port, cases, q):
     sys.path.insert(0, str(ROOT))
     import torch.distributed as dist
@@ -47,7 +57,10 @@ def _worker(rank, world, port, cases, q):
 
     out = []
     for alg, a in cases:
-        out.append(sharded_permanent(a, alg=alg, partial_fn=oracle_partial))
+        if a.dtype.kind == "i":
+            out.append(sharded_permanent(a, alg=alg, partial_fn=oracle_int_partial, exact="int128"))
+        else:
+            out.append(sharded_permanent(a, alg=alg, partial_fn=oracle_partial))
     q.put((rank, out))
     dist.barrier()
     dist.destroy_process_group()
@@ -60,7 +73,9 @@ def test_sharded_combine_gloo(world):
     g = np.random.default_rng(7)
     cases = [("glynn", g.uniform(-1, 1, (11, 11))), ("ryser", g.uniform(-1, 1, (10, 10))),
              ("glynn", g.uniform(-1, 1, (9, 9)) + 1j * g.uniform(-1, 1, (9, 9))),
-             ("ryser", g.uniform(-1, 1, (4, 9))), ("glynn", g.uniform(-1, 1, (3, 3)))]
+             ("ryser", g.uniform(-1, 1, (4, 9))), ("glynn", g.uniform(-1, 1, (3, 3))),
+             ("glynn", g.integers(-2, 3, (10, 10))), ("ryser", g.integers(0, 2, (9, 9))),
+             ("ryser", g.integers(-3, 4, (5, 9))), ("glynn", g.integers(0, 5, (4, 7)))]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -72,7 +87,11 @@ def test_sharded_combine_gloo(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     for i, (alg, a) in enumerate(cases):
-        ref = O.permanent("ryser", a)[0]
         vals = [results[r][i] for r in range(world)]
+        if a.dtype.kind == "i":
+            assert all(v == vals[0] for v in vals)
+            assert vals[0] == O.exact_int128("ryser", a)  # exact (oracle int128 walk)
+            continue
+        ref = O.permanent("ryser", a)[0]
         assert all(v == vals[0] for v in vals)  # identical on every rank
         assert abs(vals[0] - ref) <= 1e-12 * max(1.0, abs(ref))
