@@ -191,10 +191,15 @@ def run_engine(args):
         else:
             gathered.copy_(part)
 
-    # FP64-pipe roofline denominator, measured live on this GPU
+    # FP64-pipe roofline denominators, measured live on this GPU: DFMA chains
+    # (the metric's "FMA peak") and DADD/DMUL chains (the walk's own mix,
+    # which reaches the nominal rate); the roofline uses the larger
     peak = _lib.out_buf(1)
-    _lib.check(lib.perm_fp64_peak_probe(1.0, peak), "peak probe")
+    _lib.check(lib.perm_fp64_pipe_probe(0, 1.0, peak), "peak probe")
     peak_dfma = float(peak[0])
+    _lib.check(lib.perm_fp64_pipe_probe(1, 1.0, peak), "peak probe")
+    peak_addmul = float(peak[0])
+    peak_pipe = max(peak_dfma, peak_addmul)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -277,11 +282,15 @@ def run_engine(args):
                        "l2": "flushed (256 MiB write) before every step, outside the timed events",
                        "launch": {"grid": grid.value, "threads": 256, "log2_chunk": log2L.value},
                        "value_check": value_check},
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_dfma, "unit": "FP64 op/s",
-                         "frac": achieved / peak_dfma, "frac_of_nominal": achieved / NOMINAL_DFMA,
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_pipe, "unit": "FP64 op/s",
+                         "frac": achieved / peak_pipe, "frac_of_fma_peak": achieved / peak_dfma,
+                         "frac_of_nominal": achieved / NOMINAL_DFMA,
+                         "peak_dfma": peak_dfma, "peak_dadd_dmul": peak_addmul,
                          "traffic": traffic,
-                         "peak_source": "live DFMA probe on this GPU (perm_fp64_peak_probe; MEASURED_PEAKS.json "
-                                        "has no FP64 entry); nominal = 148 SM x 64 DFMA/clk x 1965 MHz",
+                         "peak_source": "measured live on this GPU, max of two FP64-pipe probes "
+                                        "(perm_fp64_pipe_probe: DFMA chains, DADD/DMUL chains); "
+                                        "MEASURED_PEAKS.json has no FP64 entry; nominal = 148 SM x 64 "
+                                        "op/clk x 1965 MHz",
                          "ops_per_step": 2 * n, "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / (t_ms / args.steps)},
             "cpu_baseline": cpu,
@@ -290,7 +299,7 @@ def run_engine(args):
                     "d2h_bytes_per_step": 8 * 8,
                     "api": "paper_2510_03421_b200.glynn(numpy) / sharded_permanent(numpy) for N>1",
                     "s_per_permanent": float(e2e.item()) / args.steps},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": args.steps,  # one walk_kernel per step (block partials combined in-kernel)
             "clocks": clocks,
         }
         print(json.dumps(line))

@@ -62,6 +62,10 @@ int perm_last_kernel_plan(int* grid, int* log2L);
 /* FP64-pipe roofline denominator: DFMA/s sustained by an 8-chain DFMA
  * kernel over the whole device for about `seconds`. */
 int perm_fp64_peak_probe(double seconds, double* dfma_per_s);
+/* op 0: DFMA (as above); op 1: alternating DADD / DMUL chains, the walk's
+ * instruction mix -- on B200 it reaches the nominal 64 op/clk/SM while DFMA
+ * tops out ~8% lower, so the walk's FP64-pipe roofline is op 1's figure. */
+int perm_fp64_pipe_probe(int op, double seconds, double* ops_per_s);
 
 /* ---- single permanents, float64 / complex128 --------------------------
  * Replace glynn_sq/glynn_rect + permanent_glynn_{square,rectangular}

@@ -321,7 +321,12 @@ int perm_last_kernel_plan(int* grid, int* log2L) {
 
 int perm_fp64_peak_probe(double seconds, double* dfma_per_s) {
   clear_error();
-  return fp64_peak_probe(seconds, dfma_per_s);
+  return fp64_peak_probe(seconds, 0, dfma_per_s);
+}
+
+int perm_fp64_pipe_probe(int op, double seconds, double* ops_per_s) {
+  clear_error();
+  return fp64_peak_probe(seconds, op, ops_per_s);
 }
 
 int perm_device_sm_count(void) {

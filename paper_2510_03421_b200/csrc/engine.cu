@@ -244,22 +244,37 @@ KernelTimer& kernel_timer() {
   return t;
 }
 
-// FP64-pipe probe: 8 independent DFMA chains per thread over a full grid.
-__global__ void dfma_probe_kernel(double* out, int iters, double a, double b) {
-  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
-         x7 = x0 + 7;
-  for (int i = 0; i < iters; ++i) {
+// FP64-pipe probes over a full grid, 8 independent chains per thread:
+// OP 0 = DFMA (the metric's "FMA peak"), OP 1 = alternating DADD / DMUL (the
+// walk's instruction mix).  On B200 the second runs at the nominal 64/clk/SM,
+// the first ~8% lower (three-operand reads), so the walk's roofline
+// denominator is the larger of the two.
+template <int OP>
+__global__ void fp64_probe_kernel(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
-      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if constexpr (OP == 0) x[i] = fma(x[i], a, b);
+        else x[i] = (i & 1) ? x[i] * a : x[i] + b;
+      }
     }
   }
-  const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
   if (s == 12345.678) out[0] = s;
 }
 
-int fp64_peak_probe(double seconds, double* dfma_per_s) {
+int fp64_peak_probe(double seconds, int op, double* ops_per_s) {
+  if (op != 0 && op != 1) {
+    set_error("probe op must be 0 (DFMA) or 1 (DADD/DMUL)");
+    return PERM_BAD_ARG;
+  }
   int dev = 0, nsm = 148;
   PERM_CUDA_TRY(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -270,25 +285,27 @@ int fp64_peak_probe(double seconds, double* dfma_per_s) {
   cudaEventCreate(&e1);
   const int blocks = nsm * 4, threads = 512, iters = 2048;
   const double per_launch = (double)blocks * threads * iters * 16 * 8;
-  dfma_probe_kernel<<<blocks, threads>>>(d, iters, 0.999, 1e-3);  // warm-up
+  auto kern = op == 0 ? fp64_probe_kernel<0> : fp64_probe_kernel<1>;
+  const double a = op == 0 ? 0.999 : 0.999999, b = op == 0 ? 1e-3 : 1e-9;
+  kern<<<blocks, threads>>>(d, iters, a, b);  // warm-up
   cudaEventRecord(e0);
-  dfma_probe_kernel<<<blocks, threads>>>(d, iters, 0.999, 1e-3);
+  kern<<<blocks, threads>>>(d, iters, a, b);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   int reps = (int)std::max(1.0, seconds / std::max(1e-6, ms * 1e-3));
   cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) dfma_probe_kernel<<<blocks, threads>>>(d, iters, 0.999, 1e-3);
+  for (int r = 0; r < reps; ++r) kern<<<blocks, threads>>>(d, iters, a, b);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   cudaEventElapsedTime(&ms, e0, e1);
-  *dfma_per_s = per_launch * reps / (ms * 1e-3);
+  *ops_per_s = per_launch * reps / (ms * 1e-3);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(d);
   const cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? PERM_OK : cuda_fail(e, "dfma probe");
+  return e == cudaSuccess ? PERM_OK : cuda_fail(e, "fp64 probe");
 }
 
 // ---------------------------------------------------------------- kernels

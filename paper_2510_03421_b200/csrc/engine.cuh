@@ -85,6 +85,6 @@ struct KernelTimer {
 KernelTimer& kernel_timer();
 bool timing_enabled();
 void set_timing(bool on);
-int fp64_peak_probe(double seconds, double* dfma_per_s);
+int fp64_peak_probe(double seconds, int op, double* ops_per_s);
 
 }  // namespace permb200

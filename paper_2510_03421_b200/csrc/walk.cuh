@@ -260,6 +260,9 @@ __device__ __forceinline__ T chain_product(const T (&v)[P]) {
 // maximal occupancy); large complex vectors get the whole register file.
 template <typename T, int P>
 __host__ __device__ constexpr int walk_min_blocks() {
+#ifdef WALK_MINB
+  return WALK_MINB;
+#endif
   return (Num<T>::kDoubles == 1) ? ((P <= 20) ? 3 : (P <= 44) ? 2 : 1) : ((P <= 14) ? 2 : 1);
 }
 

@@ -41,12 +41,12 @@ constexpr int kMaxPartials = 148 * 16;
 // chunk costing L steps plus ~3 steps' worth of seeding (6 row FMAs + the
 // warp-cooperative column sums); pick the L = 2^r (8 <= L <= 2^14) that
 // minimizes the slowest warp's work.
-inline int choose_log2L(uint64_t steps, uint64_t lanes) {
+inline int choose_log2L(uint64_t steps, uint64_t lanes, int per_group = 32) {
   const uint64_t warps = lanes / 32 ? lanes / 32 : 1;
   int best = 3;
   double best_cost = 1e300;
   for (int r = 3; r <= 14; ++r) {
-    const uint64_t groups = (steps >> r) / 32;
+    const uint64_t groups = (steps >> r) / per_group;
     if (groups < 1) break;
     const uint64_t per_warp = (groups + warps - 1) / warps;
     const double cost = (double)per_warp * ((double)(1ull << r) + 3.0);

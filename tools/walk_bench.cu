@@ -19,7 +19,7 @@ double run(int B, int reps) {
   cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
   WalkJob job{};
   job.P = P; job.B = B; job.v0 = d; job.U = d + P * w; job.mag = 0;
-  job.k_begin = 0; job.k_end = 1ull << B; job.partials = parts;
+  job.k_begin = 0; job.k_end = 1ull << B; job.partials = parts; job.final_out = parts + (size_t)(kMaxPartials - 1) * kPartialStride; { static unsigned int* dn = nullptr; if (!dn) { cudaMalloc(&dn, 4); cudaMemset(dn, 0, 4); } job.done = dn; }
   WalkPlan plan;
   launch_walk<T, P, false>(job, &plan, 0);
   cudaDeviceSynchronize();
@@ -36,7 +36,16 @@ double run(int B, int reps) {
   cudaFree(d); cudaFree(parts);
   return ms;
 }
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == '3') {  // P = 36 only (profiling)
+    run<double, 36>(35, 1);
+    return 0;
+  }
+  if (argc > 1) {  // quick functional check
+    run<double, 28>(20, 1);
+    run<cd, 24>(18, 1);
+    return 0;
+  }
   run<double, 36>(35, 3);
   run<double, 32>(31, 10);
   run<double, 28>(27, 20);

@@ -18,7 +18,7 @@ void one(int B) {
   cudaMalloc(&parts, kMaxPartials * kPartialStride * 8);
   cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
   WalkJob job{};
-  job.P = P; job.B = B; job.v0 = d; job.U = d + P * w; job.k_begin = 0; job.k_end = 1ull << B; job.partials = parts;
+  job.P = P; job.B = B; job.v0 = d; job.U = d + P * w; job.k_begin = 0; job.k_end = 1ull << B; job.partials = parts; job.final_out = parts + (size_t)(kMaxPartials - 1) * kPartialStride; { static unsigned int* dn = nullptr; if (!dn) { cudaMalloc(&dn, 4); cudaMemset(dn, 0, 4); } job.done = dn; }
   WalkPlan plan;
   launch_walk<T, P, false>(job, &plan, 0);
   cudaDeviceSynchronize();

@@ -17,7 +17,7 @@ void sweep(int B) {
   for (int r = 0; r <= 0; ++r) {
     WalkJob job{};
     job.P = P; job.B = B; job.v0 = d; job.U = d + P; job.k_begin = 0; job.k_end = 1ull << B;
-    job.partials = parts; job.force_log2L = r;
+    job.partials = parts; job.final_out = parts + (size_t)(kMaxPartials - 1) * kPartialStride; { static unsigned int* dn = nullptr; if (!dn) { cudaMalloc(&dn, 4); cudaMemset(dn, 0, 4); } job.done = dn; } job.force_log2L = r;
     WalkPlan plan;
     launch_walk<double, P, false>(job, &plan, 0);
     cudaDeviceSynchronize();
