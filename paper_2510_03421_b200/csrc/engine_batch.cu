@@ -1,6 +1,9 @@
 // Host side of the batched small-matrix kernels (perm_batch_*).
 #include <algorithm>
 #include <cstring>
+#include <condition_variable>
+#include <cstdlib>
+#include <mutex>
 #include <thread>
 #include <utility>
 #include <vector>
@@ -193,23 +196,72 @@ static BatchPipe& batch_pipe() {
   return g_pipe[dev & 15];
 }
 
-// Host memcpy split over a few threads (pageable -> pinned staging).
+// Host memcpy split over persistent threads (pageable -> pinned staging).
+// Spawning threads per chunk cost ~0.1 ms per chunk; the pool is created on
+// first use and lives for the process.  One copy at a time (call_mu).
+class CopyPool {
+ public:
+  void copy(void* dst, const void* src, size_t bytes, int nparts) {
+    std::lock_guard<std::mutex> call(call_mu_);
+    std::unique_lock<std::mutex> lk(mu_);
+    while ((int)nthreads_ < nparts) {
+      const int id = (int)nthreads_++;
+      std::thread([this, id] { work(id); }).detach();
+    }
+    dst_ = static_cast<char*>(dst);
+    src_ = static_cast<const char*>(src);
+    bytes_ = bytes;
+    nparts_ = nparts;
+    remaining_ = (int)nthreads_;
+    ++gen_;
+    cv_.notify_all();
+    done_.wait(lk, [this] { return remaining_ == 0; });
+  }
+
+ private:
+  void work(int id) {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      char* d = dst_;
+      const char* s = src_;
+      const size_t b = bytes_;
+      const int np = nparts_;
+      lk.unlock();
+      if (id < np) {
+        const size_t part = ((b + np - 1) / np + 4095) & ~(size_t)4095;
+        const size_t off = (size_t)id * part;
+        if (off < b) std::memcpy(d + off, s + off, std::min(part, b - off));
+      }
+      lk.lock();
+      if (--remaining_ == 0) done_.notify_all();
+    }
+  }
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_;
+  size_t nthreads_ = 0;
+  uint64_t gen_ = 0;
+  int remaining_ = 0, nparts_ = 0;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
 static void par_memcpy(void* dst, const void* src, size_t bytes) {
-  const size_t kMin = 8u << 20;
-  if (bytes < kMin) {
+  static CopyPool* pool = new CopyPool();  // detached workers: never destroyed
+  const int nt = std::max(1, std::min(32, env_int("PERM_COPY_THREADS", 8)));
+  if (bytes < (4u << 20) || nt == 1) {
     std::memcpy(dst, src, bytes);
     return;
   }
-  const int nt = 4;
-  std::vector<std::thread> th;
-  const size_t part = (bytes + nt - 1) / nt;
-  for (int i = 0; i < nt; ++i) {
-    const size_t off = (size_t)i * part;
-    if (off >= bytes) break;
-    const size_t len = std::min(part, bytes - off);
-    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len); });
-  }
-  for (auto& t : th) t.join();
+  pool->copy(dst, src, bytes, nt);
 }
 
 int batch_select(int m, int n) {
@@ -250,7 +302,8 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
   // the kernels overlap (the input is read from pageable numpy memory).
   Scratch* sc = scratch();
   if (!sc) return cuda_fail(cudaErrorNoDevice, "scratch");
-  int64_t chunk = std::max<int64_t>(1, (int64_t)((32u << 20) / mat_bytes));
+  const size_t chunk_bytes = (size_t)std::max(1, env_int("PERM_BATCH_CHUNK_MB", 32)) << 20;
+  int64_t chunk = std::max<int64_t>(1, (int64_t)(chunk_bytes / mat_bytes));
   chunk = std::min<int64_t>(chunk, B);
   const size_t in_chunk = (size_t)chunk * mat_bytes, out_chunk = (size_t)chunk * esz;
   BatchPipe& bp = batch_pipe();
