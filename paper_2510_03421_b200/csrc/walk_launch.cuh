@@ -1,5 +1,6 @@
 // Host-side planning and launch of the Gray-walk kernels.
 #pragma once
+#include <atomic>
 #include <utility>
 
 #include "walk.cuh"
@@ -73,12 +74,27 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
     if (e != cudaSuccess) return e;
     attr_smem = (int)smem;
   }
-  int dev = 0, nsm = 148, bps = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kWalkThreads, smem);
-  if (e != cudaSuccess) return e;
-  if (bps < 1) bps = 1;
+  int nsm = 148, bps = 1;
+  {
+    // occupancy depends only on (kernel, dynamic smem): cache the last answer
+    // (the query costs microseconds, comparable to a whole n <= 22 walk)
+    static std::atomic<uint64_t> cache{0};  // smem << 32 | dev << 24 | bps << 12 | nsm; 0 = empty
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t c = cache.load(std::memory_order_relaxed);
+    if (c && (c >> 32) == smem && (int)((c >> 24) & 0xff) == dev) {
+      bps = (int)((c >> 12) & 0xfff);
+      nsm = (int)(c & 0xfff);
+    } else {
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kWalkThreads, smem);
+      if (e != cudaSuccess) return e;
+      if (bps < 1) bps = 1;
+      cache.store(((uint64_t)smem << 32) | ((uint64_t)(dev & 0xff) << 24) | ((uint64_t)(bps & 0xfff) << 12) |
+                      (uint64_t)(nsm & 0xfff),
+                  std::memory_order_relaxed);
+    }
+  }
   if (bps * nsm > kMaxPartials) bps = kMaxPartials / nsm;
   const uint64_t lanes = (uint64_t)bps * nsm * kWalkThreads;
   // alignment: chunks of L must tile [k_begin, k_end) in groups of 32
