@@ -95,8 +95,13 @@ int perm_comb_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, uint6
                   void* stream);
 int perm_comb_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t step_budget, double* out,
                    void* stream);
-int perm_comb_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, uint64_t step_budget, int64_t* out,
-                  void* stream);
+/* Integer combinatoric: width 64 = comb_dfs_int (src/_kernels.py:59-108)
+ * with its checked-int64 overflow semantics (PERM_OVERFLOW exactly where the
+ * reference reports overflowed); width 128 = exact DFS in int128, certified a
+ * priori (product of the row sums of |A| < 2^126, else PERM_OVERFLOW).
+ * out[0], out[1] = low, high 64 bits; *fits_int64 set (may be NULL). */
+int perm_comb_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, uint64_t step_budget,
+                  int64_t* out, int* fits_int64, void* stream);
 
 /* ---- exact integer path (north_star item 3) -----------------------------
  * width = 64: the reference's checked-int64 semantics bit for bit

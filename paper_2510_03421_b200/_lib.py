@@ -42,7 +42,8 @@ SIGNATURES = {
     "perm_ryser_c128": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _dp, _vp]),
     "perm_comb_f64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_uint64, _dp, _vp]),
     "perm_comb_c128": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_uint64, _dp, _vp]),
-    "perm_comb_i64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_uint64, _ip, _vp]),
+    "perm_comb_i64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, C.c_uint64, _ip,
+                                C.POINTER(C.c_int), _vp]),
     "perm_glynn_i64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, _ip,
                                  C.POINTER(C.c_int), _vp]),
     "perm_ryser_i64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, _ip,

@@ -63,14 +63,18 @@ def _int_walk(alg: str, a: Matrix, exact) -> PermanentResult:
 
 
 def permanent_combinatoric(a: Matrix, step_budget: int = DEFAULT_STEP_BUDGET,
-                           compiled=None) -> PermanentResult:
-    """Sum over all m-permutations of the columns (src/algorithms.py:71-90)."""
+                           compiled=None, exact=None) -> PermanentResult:
+    """Sum over all m-permutations of the columns (src/algorithms.py:71-90).
+    Integer matrices: checked int64 by default, ``exact="int128"`` for the
+    exact int128 DFS (a-priori certified)."""
     _need(a.m <= a.n, f"need m <= n, got {a.m}x{a.n}; transpose first")
+    if exact not in _EXACT_MODES:
+        raise ValueError(f"exact must be one of {_EXACT_MODES}, got {exact!r}")
     perms = math.perm(a.n, a.m)
     if perms > step_budget:
         raise StepBudgetExceeded(
             f"combinatoric on {a.m}x{a.n} needs {perms} permutations (> budget {step_budget})")
-    value, ovf, _ = engine.comb(a.data, step_budget)
+    value, ovf, _ = engine.comb(a.data, step_budget, width=128 if exact == "int128" else 64)
     if a.kind is ElementKind.INT64:
         return PermanentResult(int(value), bool(ovf))
     return _float_result(value, a.kind)
@@ -119,7 +123,7 @@ def run_algorithm(a: Matrix, alg: AlgorithmId, compiled=None,
     """One algorithm on an m <= n matrix, square or rectangular form by shape
     (src/algorithms.py:187-201)."""
     if alg is AlgorithmId.COMBINATORIC:
-        return permanent_combinatoric(a, step_budget=step_budget, compiled=compiled)
+        return permanent_combinatoric(a, step_budget=step_budget, compiled=compiled, exact=exact)
     if alg is AlgorithmId.RYSER:
         if a.m == a.n:
             return permanent_ryser_square(a, compiled=compiled, exact=exact)

@@ -382,9 +382,18 @@ int perm_comb_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, uint
                    void* stream) {
   return comb_permanent(false, 1, m, n, a, lda, dev_ptr, step_budget, out, nullptr, stream);
 }
-int perm_comb_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, uint64_t step_budget, int64_t* out,
-                  void* stream) {
-  return comb_permanent(false, 2, m, n, a, lda, dev_ptr, step_budget, nullptr, out, stream);
+int perm_comb_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, uint64_t step_budget,
+                  int64_t* out, int* fits_int64, void* stream) {
+  if (width != 64 && width != 128) {
+    clear_error();
+    set_error("width must be 64 or 128");
+    return PERM_BAD_ARG;
+  }
+  int st = comb_permanent(false, width == 64 ? 2 : 3, m, n, a, lda, dev_ptr, step_budget, nullptr, out, stream);
+  if (st) return st;
+  if (width == 64) out[1] = out[0] < 0 ? -1 : 0;
+  if (fits_int64) *fits_int64 = (out[1] == (out[0] < 0 ? -1 : 0)) ? 1 : 0;
+  return PERM_OK;
 }
 
 int perm_batch_f64(int alg, int64_t B, int m, int n, const double* a, double* out, int dev_ptr, void* stream) {

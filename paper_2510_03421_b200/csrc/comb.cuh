@@ -22,7 +22,7 @@ namespace permb200 {
 
 constexpr int kCombThreads = 128;
 
-enum CombMode { kCombF64 = 0, kCombC128 = 1, kCombI64 = 2 };
+enum CombMode { kCombF64 = 0, kCombC128 = 1, kCombI64 = 2, kCombI128 = 3 };
 
 struct CombArgs {
   const void* a;          // m x n row-major (double / cd / int64)
@@ -197,17 +197,39 @@ __global__ void __launch_bounds__(kCombThreads) ryser_comb_kernel(CombArgs A) {
 // ---------------------------------------------------------------- combinatoric
 // Prefix of depth D with lexicographic index `idx` among the P(n, D)
 // D-permutations: digit q picks the (idx_q)-th unused column.
+// MODE kCombI128: exact wrapping int128 products and sums (the host only
+// launches it when an a-priori bound keeps every prefix product and partial
+// sum inside int128, so the zero pruning sees true zeros).
 template <int MODE>
 __global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
   const int m = A.m, n = A.n, D = A.depth;
   const uint64_t gtid = (uint64_t)blockIdx.x * kCombThreads + threadIdx.x;
+  constexpr bool kInt = (MODE == kCombI64 || MODE == kCombI128);
   double hi = 0, lo = 0, hi_i = 0, lo_i = 0;
   Summ sm;
   sm.S = i128_from(0); sm.mn = i128_from(0); sm.mx = i128_from(0); sm.flag = 0;
+  i128 wide = i128_from(0);  // kCombI128 running sum (mod 2^128)
   bool have = false;
-  using T = typename std::conditional<MODE == kCombF64, double,
-                                      typename std::conditional<MODE == kCombC128, cd, int64_t>::type>::type;
-  const T* a = static_cast<const T*>(A.a);
+  // element type of the matrix, and of the prefix products
+  using Te = typename std::conditional<MODE == kCombF64, double,
+                                       typename std::conditional<MODE == kCombC128, cd, int64_t>::type>::type;
+  using T = typename std::conditional<MODE == kCombI128, i128, Te>::type;
+  const Te* a = static_cast<const Te*>(A.a);
+  auto is_zero = [](const T& p) -> bool {
+    if constexpr (MODE == kCombI128) return (p.lo | p.hi) == 0;
+    else if constexpr (MODE == kCombI64) return p == 0;
+    else if constexpr (MODE == kCombF64) return p == 0.0;
+    else return p.x == 0.0 && p.y == 0.0;
+  };
+  auto leaf = [&](const T& p) {
+    if constexpr (MODE == kCombI64) {
+      sm.S = i128_add(sm.S, i128_from(p));
+      if (!have) { sm.mn = sm.S; sm.mx = sm.S; have = true; }
+      else { if (i128_lt(sm.S, sm.mn)) sm.mn = sm.S; if (i128_lt(sm.mx, sm.S)) sm.mx = sm.S; }
+    } else if constexpr (MODE == kCombI128) {
+      wide = i128_add(wide, p);
+    }
+  };
   const uint64_t p0 = gtid * A.per_thread;
   uint64_t p1 = p0 + A.per_thread;
   if (p1 > A.total) p1 = A.total;
@@ -238,7 +260,9 @@ __global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
     // prefix products (checked / pruned exactly like the reference DFS)
     T prod[65];
     bool dead = false;
-    if constexpr (MODE == kCombI64) prod[0] = 1; else prod[0] = Num<T>::one();
+    if constexpr (MODE == kCombI64) prod[0] = 1;
+    else if constexpr (MODE == kCombI128) prod[0] = i128_from(1);
+    else prod[0] = Num<T>::one();
     for (int q = 0; q < D; ++q) {
       T p;
       if constexpr (MODE == kCombI64) {
@@ -247,14 +271,14 @@ __global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
         } else {
           p = prod[q] * a[q * n + choice[q]];
         }
+      } else if constexpr (MODE == kCombI128) {
+        p = i128_mul_s64(prod[q], a[q * n + choice[q]]);
       } else {
         p = Num<T>::mul(prod[q], a[q * n + choice[q]]);
       }
       if (q == m - 1) {  // leaf inside the prefix (D == m)
-        if constexpr (MODE == kCombI64) {
-          sm.S = i128_add(sm.S, i128_from(p));
-          if (!have) { sm.mn = sm.S; sm.mx = sm.S; have = true; }
-          else { if (i128_lt(sm.S, sm.mn)) sm.mn = sm.S; if (i128_lt(sm.mx, sm.S)) sm.mx = sm.S; }
+        if constexpr (kInt) {
+          leaf(p);
         } else {
           dd_acc(hi, lo, Num<T>::re(p));
           dd_acc(hi_i, lo_i, Num<T>::im(p));
@@ -262,11 +286,7 @@ __global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
         dead = true;
         break;
       }
-      bool zero;
-      if constexpr (MODE == kCombI64) zero = (p == 0);
-      else if constexpr (MODE == kCombF64) zero = (p == 0.0);
-      else zero = (p.x == 0.0 && p.y == 0.0);
-      if (zero) { dead = true; break; }  // src/_kernels.py:52 prune
+      if (is_zero(p)) { dead = true; break; }  // src/_kernels.py:52 prune
       prod[q + 1] = p;
     }
     if (dead) continue;
@@ -274,8 +294,8 @@ __global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
     int ch[64];
     for (int q = 0; q < m; ++q) ch[q] = -1;
     int d = D;
-    T chunk;
-    if constexpr (MODE == kCombI64) chunk = 0; else chunk = Num<T>::zero();
+    Te chunk;
+    if constexpr (kInt) chunk = 0; else chunk = Num<Te>::zero();
     while (d >= D) {
       int j = ch[d];
       if (j >= 0) used[j] = false;
@@ -286,32 +306,23 @@ __global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
       T p;
       if constexpr (MODE == kCombI64) {
         if (mul_ovf(prod[d], a[d * n + j], p)) { sm.flag = 1; break; }
+      } else if constexpr (MODE == kCombI128) {
+        p = i128_mul_s64(prod[d], a[d * n + j]);
       } else {
         p = Num<T>::mul(prod[d], a[d * n + j]);
       }
       if (d == m - 1) {
-        if constexpr (MODE == kCombI64) {
-          sm.S = i128_add(sm.S, i128_from(p));
-          if (!have) { sm.mn = sm.S; sm.mx = sm.S; have = true; }
-          else { if (i128_lt(sm.S, sm.mn)) sm.mn = sm.S; if (i128_lt(sm.mx, sm.S)) sm.mx = sm.S; }
-        } else {
-          chunk = Num<T>::add(chunk, p);
-        }
-      } else {
-        bool zero;
-        if constexpr (MODE == kCombI64) zero = (p == 0);
-        else if constexpr (MODE == kCombF64) zero = (p == 0.0);
-        else zero = (p.x == 0.0 && p.y == 0.0);
-        if (!zero) {
-          used[j] = true;
-          prod[d + 1] = p;
-          ++d;
-        }
+        if constexpr (kInt) leaf(p);
+        else chunk = Num<T>::add(chunk, p);
+      } else if (!is_zero(p)) {
+        used[j] = true;
+        prod[d + 1] = p;
+        ++d;
       }
     }
-    if constexpr (MODE != kCombI64) {
-      dd_acc(hi, lo, Num<T>::re(chunk));
-      dd_acc(hi_i, lo_i, Num<T>::im(chunk));
+    if constexpr (!kInt) {
+      dd_acc(hi, lo, Num<Te>::re(chunk));
+      dd_acc(hi_i, lo_i, Num<Te>::im(chunk));
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -340,6 +351,19 @@ __global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
       o[2] = (int64_t)t.mn.lo; o[3] = (int64_t)t.mn.hi;
       o[4] = (int64_t)t.mx.lo; o[5] = (int64_t)t.mx.hi;
       o[6] = t.flag; o[7] = 0;
+    }
+  } else if constexpr (MODE == kCombI128) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) wide = i128_add(wide, shfl_down_i128(wide, off));
+    __shared__ i128 wsum[kCombThreads / 32];
+    if (lane == 0) wsum[warp] = wide;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      i128 t = wsum[0];
+      for (int w = 1; w < kCombThreads / 32; ++w) t = i128_add(t, wsum[w]);
+      int64_t* o = static_cast<int64_t*>(A.out) + (size_t)blockIdx.x * 8;
+      o[0] = (int64_t)t.lo; o[1] = (int64_t)t.hi;
+      for (int q = 2; q < 8; ++q) o[q] = 0;
     }
   } else {
 #pragma unroll

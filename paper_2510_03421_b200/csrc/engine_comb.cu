@@ -117,8 +117,10 @@ static void combine_float(const std::vector<int64_t>& h, double* re_h, double* r
   }
 }
 
-// mode 0 f64, 1 c128, 2 int64 checked.  Float: out[0..1] = re, im.
-// Int: *ivalue, PERM_OVERFLOW on reference overflow.
+// mode 0 f64, 1 c128, 2 int64 checked, 3 exact int128 (combinatoric only).
+// Float: out[0..1] = re, im.  Mode 2: *ivalue, PERM_OVERFLOW on reference
+// overflow.  Mode 3: ivalue[0..1] = lo, hi; PERM_OVERFLOW when the a-priori
+// bound (product of the row sums of |A|) does not certify int128.
 int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t lda, int dev_ptr,
                    uint64_t step_budget, double* out, int64_t* ivalue, void* stream_) {
   clear_error();
@@ -136,6 +138,10 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
       set_error("combinatoric step budget exceeded");
       return PERM_BUDGET;
     }
+  }
+  if (mode == 3 && ryser) {
+    set_error("exact int128 combination-order Ryser is not provided; use the int128 walk");
+    return PERM_BAD_ARG;
   }
   cudaStream_t stream = pick_stream(stream_);
   const int esz = (mode == 1) ? 16 : 8;
@@ -225,7 +231,33 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
     while (D < m && nperm(n, D) < thr * 4) ++D;
     if (D < 1) D = 1;
     const uint64_t total = nperm(n, D);
-    if (mode == 2) {
+    if (mode == 3) {
+      // every prefix product and partial sum is bounded by prod_i max(1, sum_j |a_ij|)
+      long double bound = 1.0L;
+      for (int i = 0; i < m; ++i) {
+        long double r = 0;
+        for (int j = 0; j < n; ++j) {
+          int64_t x;
+          std::memcpy(&x, &hA[((size_t)i * n + j) * 8], 8);
+          r += std::fabs((long double)x);
+        }
+        bound *= std::max(1.0L, r);
+      }
+      if (!(bound < std::ldexp(1.0L, 126))) {
+        set_error("exact value not certified to fit int128 (product of the row sums of |A| >= 2^126)");
+        return PERM_OVERFLOW;
+      }
+      uint64_t nb = 0;
+      st = enqueue_comb<kCombI128>(false, dA, dB, m, n, 0, D, total, dOut, &nb, stream);
+      if (st) return st;
+      st = fetch_partials(dOut, nb, &h, stream);
+      if (st) return st;
+      unsigned __int128 acc = 0;
+      for (uint64_t b = 0; b < nb; ++b)
+        acc += ((unsigned __int128)(uint64_t)h[b * 8 + 1] << 64) | (uint64_t)h[b * 8];
+      ivalue[0] = (int64_t)(uint64_t)acc;
+      ivalue[1] = (int64_t)(uint64_t)(acc >> 64);
+    } else if (mode == 2) {
       uint64_t nb = 0;
       st = enqueue_comb<kCombI64>(false, dA, dB, m, n, 0, D, total, dOut, &nb, stream);
       if (st) return st;

@@ -52,10 +52,12 @@ def walk(alg: str, a, magsum: bool = False):
     return val, (mg.value if magsum else None)
 
 
-def comb(a, step_budget: int):
-    """Combinatoric permanent (float64 / complex128 / checked int64).
-    Returns (value, overflowed); raises ValueError / RuntimeError codes as the
-    C ABI reports them (BUDGET is mapped by the caller)."""
+def comb(a, step_budget: int, width: int = 64):
+    """Combinatoric permanent (float64 / complex128 / integer).
+    Returns (value, overflowed, status).  Integers: width=64 is the
+    reference's checked int64 (overflowed as it reports it); width=128 the
+    exact int128 DFS, overflowed = "does not fit int64", OverflowError when
+    the int128 bound fails.  BUDGET is mapped by the caller."""
     lib = _lib.load()
     m, n = a.shape
     kind = a.dtype.kind if isinstance(a, np.ndarray) else None
@@ -63,13 +65,17 @@ def comb(a, step_budget: int):
     budget = C.c_uint64(min(int(step_budget), (1 << 64) - 1) if step_budget >= 0 else 0)
     if kind in ("i",):
         out = (C.c_int64 * 2)()
-        st = lib.perm_comb_i64(m, n, ptr, lda, dev, budget, out, stream)
+        fits = C.c_int(1)
+        st = lib.perm_comb_i64(m, n, ptr, lda, dev, width, budget, out, C.byref(fits), stream)
         if st == _lib.OVERFLOW:
-            return 0, True, st
+            if width == 64:
+                return 0, True, st
+            raise OverflowError(f"exact int128 combinatoric {m}x{n}: {_lib.last_error()}")
         if st == _lib.BUDGET:
             return None, False, st
         _lib.check(st, f"combinatoric {m}x{n}")
-        return int(out[0]), False, st
+        v = (int(out[1]) << 64) | (int(out[0]) & ((1 << 64) - 1))
+        return v, (width == 128 and not fits.value), st
     cplx = np.iscomplexobj(a)
     out = _lib.out_buf(2)
     fn = lib.perm_comb_c128 if cplx else lib.perm_comb_f64

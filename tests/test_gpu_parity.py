@@ -433,3 +433,22 @@ def test_concurrent_calls_from_threads():
     with ThreadPoolExecutor(max_workers=3) as ex:
         got = list(ex.map(lambda b: P.ryser(b, exact="int128"), ints))
     assert got == [O.exact_int128("glynn", b) for b in ints]
+
+
+def test_combinatoric_int128():
+    """perm_comb_i64 width 128: exact DFS in int128, a-priori certified."""
+    big = np.array([[2**62, 3], [5, 2**62]], dtype=np.int64)
+    assert P.combinatoric(big, exact="int128") == 2**124 + 15
+    with pytest.raises(OverflowError):
+        P.combinatoric(big)  # reference semantics unchanged
+    rng = np.random.default_rng(31)
+    for m, n in ((12, 12), (9, 11), (5, 13), (1, 7)):
+        a = rng.integers(-2, 3, (m, n)).astype(np.int64)
+        assert P.combinatoric(a, exact="int128") == O.exact_int128("ryser", a)
+    a = rng.integers(0, 1000, (5, 5)).astype(np.int64) * 10**3  # products need > 64 bits
+    assert P.combinatoric(a, exact="int128") == O.exact_int128("glynn", a)
+    huge = np.full((3, 3), 2**62, dtype=np.int64)  # bound 2^(3*63.6) >= 2^126: refused
+    with pytest.raises(OverflowError):
+        P.combinatoric(huge, exact="int128")
+    r = run_algorithm(as_matrix(big), AlgorithmId.COMBINATORIC, exact="int128")
+    assert r.value == 2**124 + 15 and r.overflowed  # value exact, flag = does not fit int64
