@@ -32,6 +32,12 @@ struct CombArgs {
   uint64_t per_thread;    // items per thread
   int depth;              // comb_dfs: prefix depth D
   void* out;              // per block partials
+  // ryser, fused launch (all subset sizes s = m..1 in one grid): block range
+  // [blk_first[s], blk_first[s] + blk_count[s]) walks the C(n, s) subsets of
+  // size s, tot[s] items, per[s] per thread
+  int fused;
+  int smem_binom, smem_matrix;  // stage binomials (rows < n, cols < m) / the matrix in shared memory
+  uint64_t blk_first[64], blk_count[64], tot[64], per[64];
 };
 
 __device__ __forceinline__ uint64_t binom_at(const uint64_t* tab, int i, int j) {
@@ -41,11 +47,47 @@ __device__ __forceinline__ uint64_t binom_at(const uint64_t* tab, int i, int j) 
 // ---------------------------------------------------------------- Ryser
 template <int MODE>
 __global__ void __launch_bounds__(kCombThreads) ryser_comb_kernel(CombArgs A) {
-  const int m = A.m, n = A.n, s = A.s;
-  const uint64_t gtid = (uint64_t)blockIdx.x * kCombThreads + threadIdx.x;
-  const uint64_t r0 = gtid * A.per_thread;
-  uint64_t r1 = r0 + A.per_thread;
-  if (r1 > A.total) r1 = A.total;
+  const int m = A.m, n = A.n;
+  int s = A.s;
+  uint64_t bid = blockIdx.x, total = A.total, per_thread = A.per_thread;
+  if (A.fused) {
+    for (int q = m; q >= 1; --q)
+      if (bid >= A.blk_first[q] && bid < A.blk_first[q] + A.blk_count[q]) {
+        bid -= A.blk_first[q];
+        s = q;
+        total = A.tot[q];
+        per_thread = A.per[q];
+        break;
+      }
+  }
+  // tiny launches are latency-bound: the binomials the unranking reads
+  // (rows < n, columns < m) and the matrix go to shared memory first
+  using Te = typename std::conditional<MODE == kCombF64, double,
+                                       typename std::conditional<MODE == kCombC128, cd, int64_t>::type>::type;
+  extern __shared__ __align__(16) unsigned char comb_smem[];
+  const uint64_t* bt = A.binom;
+  int bstride = 63;
+  const Te* abase = static_cast<const Te*>(A.a);
+  {
+    unsigned char* p = comb_smem;
+    if (A.smem_matrix) {
+      Te* sa = reinterpret_cast<Te*>(p);
+      for (int i = threadIdx.x; i < m * n; i += kCombThreads) sa[i] = abase[i];
+      abase = sa;
+      p += (((size_t)m * n * sizeof(Te)) + 15) & ~(size_t)15;
+    }
+    if (A.smem_binom) {
+      uint64_t* sb = reinterpret_cast<uint64_t*>(p);
+      for (int i = threadIdx.x; i < n * m; i += kCombThreads) sb[i] = binom_at(A.binom, i / m, i % m);
+      bt = sb;
+      bstride = m;
+    }
+    if (A.smem_matrix || A.smem_binom) __syncthreads();
+  }
+  const uint64_t gtid = bid * kCombThreads + threadIdx.x;
+  const uint64_t r0 = gtid * per_thread;
+  uint64_t r1 = r0 + per_thread;
+  if (r1 > total) r1 = total;
   int comb[64];
   // accumulators
   double hi = 0, lo = 0, hi_i = 0, lo_i = 0;
@@ -58,14 +100,15 @@ __global__ void __launch_bounds__(kCombThreads) ryser_comb_kernel(CombArgs A) {
     int x = 0;
     for (int q = 0; q < s; ++q) {
       for (;;) {
-        const uint64_t cnt = binom_at(A.binom, n - x - 1, s - q - 1);
+        const int bi = n - x - 1, bj = s - q - 1;  // 0 <= bj < m
+        const uint64_t cnt = (bi < 0 || bj > bi) ? 0ull : bt[bi * bstride + bj];
         if (r < cnt) { comb[q] = x++; break; }
         r -= cnt;
         ++x;
       }
     }
     if constexpr (MODE == kCombI64) {
-      const int64_t* a = static_cast<const int64_t*>(A.a);
+      const int64_t* a = abase;
       int64_t rs[64];
       for (int i = 0; i < m; ++i) {
         if (r0 == 0) {  // reference initial sums: sequential checked adds
@@ -114,7 +157,7 @@ __global__ void __launch_bounds__(kCombThreads) ryser_comb_kernel(CombArgs A) {
       }
     } else {
       using T = typename std::conditional<MODE == kCombF64, double, cd>::type;
-      const T* a = static_cast<const T*>(A.a);
+      const T* a = reinterpret_cast<const T*>(abase);
       T rs[64];
       for (int i = 0; i < m; ++i) {
         T acc = Num<T>::zero();

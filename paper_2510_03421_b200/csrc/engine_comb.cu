@@ -72,10 +72,56 @@ static int enqueue_comb(bool ryser, const void* dA, const uint64_t* dB, int m, i
   a.per_thread = per;
   a.depth = depth;
   a.out = dOut;
+  a.fused = 0;
+  a.smem_binom = 0;
+  a.smem_matrix = 0;
   if (ryser) ryser_comb_kernel<MODE><<<(unsigned)blocks, kCombThreads, 0, stream>>>(a);
   else comb_dfs_kernel<MODE><<<(unsigned)blocks, kCombThreads, 0, stream>>>(a);
   PERM_CUDA_TRY(cudaGetLastError());
   *nblocks = blocks;
+  return PERM_OK;
+}
+
+// All subset sizes s = m..1 of the combination-order Ryser in ONE launch
+// (blocks of size s at first[s] .. first[s] + cnt[s]); binomials and, when
+// small, the matrix are staged in shared memory.
+template <int MODE>
+static int enqueue_ryser_fused(const void* dA, const uint64_t* dB, int m, int n, size_t esz,
+                               const std::vector<uint64_t>& bt, void* dOut, std::vector<uint64_t>* first,
+                               std::vector<uint64_t>* cnt, uint64_t* nblocks, cudaStream_t stream) {
+  const uint64_t thr = (uint64_t)target_threads();
+  CombArgs a;
+  a.a = dA;
+  a.binom = dB;
+  a.m = m;
+  a.n = n;
+  a.s = 0;
+  a.total = 0;
+  a.per_thread = 1;
+  a.depth = 0;
+  a.out = dOut;
+  a.fused = 1;
+  uint64_t off = 0;
+  for (int s = m; s >= 1; --s) {
+    const uint64_t total = bt[n * 63 + s];
+    uint64_t per = (total + thr - 1) / thr;
+    if (per < 1) per = 1;
+    const uint64_t blocks = ((total + per - 1) / per + kCombThreads - 1) / kCombThreads;
+    a.blk_first[s] = off;
+    a.blk_count[s] = blocks;
+    a.tot[s] = total;
+    a.per[s] = per;
+    (*first)[s] = off;
+    (*cnt)[s] = blocks;
+    off += blocks;
+  }
+  const size_t mat = (((size_t)m * n * esz) + 15) & ~(size_t)15, bin = (size_t)m * n * 8;
+  a.smem_matrix = (mat + bin <= 40 * 1024) ? 1 : 0;
+  a.smem_binom = (bin <= 40 * 1024) ? 1 : 0;
+  const size_t smem = (a.smem_matrix ? mat : 0) + (a.smem_binom ? bin : 0);
+  ryser_comb_kernel<MODE><<<(unsigned)off, kCombThreads, smem, stream>>>(a);
+  PERM_CUDA_TRY(cudaGetLastError());
+  *nblocks = off;
   return PERM_OK;
 }
 
@@ -184,16 +230,10 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
     // all subset sizes enqueued back to back, one read-back
     std::vector<uint64_t> first(m + 2, 0), cnt(m + 2, 0);
     uint64_t off = 0;
-    for (int s = m; s >= 1; --s) {
-      const uint64_t total = bt[n * 63 + s];
-      void* dst = static_cast<int64_t*>(dOut) + off * 8;
-      st = (mode == 2) ? enqueue_comb<kCombI64>(true, dA, dB, m, n, s, 0, total, dst, &cnt[s], stream)
-           : (mode == 0) ? enqueue_comb<kCombF64>(true, dA, dB, m, n, s, 0, total, dst, &cnt[s], stream)
-                         : enqueue_comb<kCombC128>(true, dA, dB, m, n, s, 0, total, dst, &cnt[s], stream);
-      if (st) return st;
-      first[s] = off;
-      off += cnt[s];
-    }
+    st = (mode == 2) ? enqueue_ryser_fused<kCombI64>(dA, dB, m, n, esz, bt, dOut, &first, &cnt, &off, stream)
+         : (mode == 0) ? enqueue_ryser_fused<kCombF64>(dA, dB, m, n, esz, bt, dOut, &first, &cnt, &off, stream)
+                       : enqueue_ryser_fused<kCombC128>(dA, dB, m, n, esz, bt, dOut, &first, &cnt, &off, stream);
+    if (st) return st;
     std::vector<int64_t> all;
     st = fetch_partials(dOut, off, &all, stream);
     if (st) return st;

@@ -73,6 +73,26 @@ def _select(params, m, n):
     return select_algorithm(m, n, params).value
 
 
+def _regret_line(cells: dict, pos: str, neg: str, skip):
+    """Line (a, b, c) with a r + b n + c > 0 -> `pos`, else `neg`, minimizing
+    the summed slowdown over `cells` ({(m, n): {alg: s}}); None if degenerate."""
+    X, y, w = [], [], []
+    for k, t in cells.items():
+        if skip(k) or pos not in t or neg not in t:
+            continue
+        best = min(t.values())
+        ca, cb = t[pos] / best - 1.0, t[neg] / best - 1.0
+        X.append([k[0] / k[1], k[1]])
+        y.append(1.0 if ca < cb else -1.0)
+        w.append(abs(ca - cb))
+    if len(X) < 2 or len(set(y)) < 2:
+        return None
+    wv, b = _min_cost_line(np.array(X, float), np.array(y), np.array(w), angles=720)
+    if wv is None or (wv[0] == 0 and wv[1] == 0):
+        return None
+    return float(wv[0]), float(wv[1]), float(b)
+
+
 def fit_params(timings: dict, host: str = "") -> TuningParams:
     """Fit p1..p8 to measured timings {(m, n): {alg: seconds}} by minimizing
     the summed relative slowdown of the selected algorithm (grid search)."""
@@ -127,6 +147,23 @@ def fit_params(timings: dict, host: str = "") -> TuningParams:
                     c = sub_cost(p, large)
                     if c < c2:
                         b2, c2 = (p5, p6, p7), c
+            # refine each regime line with the weighted min-cost line search:
+            # for a two-way choice, the total slowdown is the regret-weighted
+            # misclassification count (weight |cost_a - cost_b|)
+            r1 = _regret_line(small, "combinatoric", "glynn", lambda k: k[0] == k[1] and k[1] <= p4)
+            if r1 is not None:
+                p = TuningParams(p1=r1[0], p2=r1[1], p3=r1[2], p4=float(p4), p5=1.0, p6=0.0, p7=-0.5,
+                                 p8=float(p8), source="machine-tuned")
+                c = sub_cost(p, small)
+                if c < c1:
+                    b1, c1 = r1, c
+            r2 = _regret_line(large, "glynn", "ryser", lambda k: False)
+            if r2 is not None:
+                p = TuningParams(p1=b1[0], p2=b1[1], p3=b1[2], p4=float(p4), p5=r2[0], p6=r2[1], p7=r2[2],
+                                 p8=float(p8), source="machine-tuned")
+                c = sub_cost(p, large)
+                if c < c2:
+                    b2, c2 = r2, c
             if c1 + c2 < best_c:
                 best_c = c1 + c2
                 best_p = TuningParams(p1=b1[0], p2=b1[1], p3=b1[2], p4=float(p4), p5=b2[0], p6=b2[1],
@@ -230,6 +267,28 @@ def time_algorithm(alg, m, n, trials=5, seed=None) -> BenchmarkSample:
             run_algorithm(mat, alg)
         ts.append((time.perf_counter() - t0) / reps)
     return BenchmarkSample(alg, m, n, m / n, statistics.median(ts), trials)
+
+
+def evaluate_dispatch(params: TuningParams, shapes, trials: int = 5, seed: int = 0):
+    """(m, n, chosen, slowdown) per probe shape, slowdown = the chosen
+    algorithm's median / the fastest feasible median, timed on the GPU engine
+    (the reference's acceptance probe, src/tuner.py:313-333)."""
+    from .algorithms import AlgorithmId
+    from .dispatch import select_algorithm
+
+    out = []
+    probe_seed = seed + 90000
+    for m, n in shapes:
+        chosen = select_algorithm(m, n, params)
+        medians = {}
+        for alg in AlgorithmId:
+            probe_seed += 1
+            smp = time_algorithm(alg, m, n, trials=trials, seed=probe_seed)
+            if smp.feasible:
+                medians[alg] = smp.median_time
+        best = min(medians.values())
+        out.append((m, n, chosen, medians[chosen] / best if chosen in medians else math.inf))
+    return out
 
 
 def label_grid(timings: dict) -> list:
