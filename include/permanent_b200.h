@@ -176,6 +176,13 @@ int perm_sharded_c128(int alg, int m, int n, const double* a, int64_t lda, int n
                       double* out, double* magsum);
 int perm_sharded_i64(int alg, int m, int n, const int64_t* a, int64_t lda, int width, int ngpu, const int* devices,
                      int64_t* out, int* fits_int64);
+/* Exchange the float drivers will use for this device list: 1 = NCCL
+ * (ncclCommInitAll clique + one grouped ncclAllGather of the partials; the
+ * default for >= 2 distinct devices when libnccl.so.2 loads), 0 = pinned
+ * host memory (a device listed twice, no NCCL, or PERM_SHARDED_EXCHANGE=host),
+ * -1 = bad arguments.  The integer driver always exchanges through the host
+ * (its partials are read back to certify the int128 fit). */
+int perm_sharded_exchange(int ngpu, const int* devices);
 
 /* ---- double-double validation walks -------------
  * Glynn or Ryser with double-double state, products and sums (~1e-30 unit

@@ -71,6 +71,7 @@ SIGNATURES = {
                                     _dp]),
     "perm_sharded_i64": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_int,
                                    C.POINTER(C.c_int), _ip, C.POINTER(C.c_int)]),
+    "perm_sharded_exchange": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
     "perm_select": (C.c_int, [C.c_int, C.c_int, _dp, C.c_int64, C.c_int]),
 }
 

@@ -2,9 +2,14 @@
 #include <algorithm>
 #include <cmath>
 #include <condition_variable>
+#include <cstdlib>
+#include <dlfcn.h>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <thread>
+
+#include <nccl.h>  // types only: the library is dlopen'ed (no link-time NCCL)
 
 #include "engine.cuh"
 
@@ -268,6 +273,142 @@ int run_shards(int alg, int m, int n, int ngpu, const int* devices,
   return PERM_OK;
 }
 
+// ---- NCCL exchange for the multi-device driver ----------------------------
+// libnccl.so.2 is opened at first use (RTLD_NOLOAD first: reuse the copy a
+// host framework such as torch already loaded), so the engine has no hard
+// NCCL dependency.  One communicator clique per distinct device list.
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*commInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!api.tried) {
+    api.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (h) {
+      api.commInitAll = reinterpret_cast<decltype(api.commInitAll)>(dlsym(h, "ncclCommInitAll"));
+      api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
+      api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(h, "ncclGroupStart"));
+      api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+      api.errStr = reinterpret_cast<decltype(api.errStr)>(dlsym(h, "ncclGetErrorString"));
+      api.ok = api.commInitAll && api.allGather && api.groupStart && api.groupEnd && api.errStr;
+    }
+  }
+  return api;
+}
+
+struct NcclClique {
+  std::vector<ncclComm_t> comms;
+  std::vector<cudaStream_t> streams;
+  std::vector<double*> part, gathered;  // per device: 8 doubles, G x 8 doubles
+};
+
+int nccl_fail(ncclResult_t r, const char* what) {
+  set_error(std::string("NCCL error '") + nccl_api().errStr(r) + "' in " + what);
+  return PERM_CUDA;
+}
+
+// communicators, streams and buffers for `devs`, created once (never freed:
+// they live as long as the process, like the engine's other scratch)
+int nccl_clique(const std::vector<int>& devs, NcclClique** out) {
+  static std::map<std::vector<int>, NcclClique*> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(devs);
+  if (it != cache.end()) {
+    *out = it->second;
+    return PERM_OK;
+  }
+  NcclApi& api = nccl_api();
+  const int G = (int)devs.size();
+  NcclClique* c = new NcclClique();
+  c->comms.resize(G);
+  ncclResult_t r = api.commInitAll(c->comms.data(), G, devs.data());
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_fail(r, "ncclCommInitAll");
+  }
+  for (int i = 0; i < G; ++i) {
+    PERM_CUDA_TRY(cudaSetDevice(devs[i]));
+    cudaStream_t st;
+    PERM_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    c->streams.push_back(st);
+    double *p = nullptr, *g = nullptr;
+    PERM_CUDA_TRY(cudaMalloc(&p, 8 * sizeof(double)));
+    PERM_CUDA_TRY(cudaMalloc(&g, (size_t)G * 8 * sizeof(double)));
+    c->part.push_back(p);
+    c->gathered.push_back(g);
+  }
+  cache[devs] = c;
+  *out = c;
+  return PERM_OK;
+}
+
+// Every device walks its shard asynchronously (device-resident partial, one
+// launch per device from this thread), one ncclAllGather of 8 doubles per
+// device inside a group, one read-back from the first device.
+int sharded_float_nccl(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int ngpu,
+                       const int* devices, double* parts) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  std::vector<int> devs(devices, devices + ngpu);
+  NcclClique* c = nullptr;
+  int st = nccl_clique(devs, &c);
+  if (st) return st;
+  for (int i = 0; i < ngpu && !st; ++i) {
+    uint64_t k0 = 0, k1 = 0;
+    st = perm_walk_shard(alg, m, n, i, ngpu, &k0, &k1);
+    if (st) break;
+    PERM_CUDA_TRY(cudaSetDevice(devs[i]));
+    st = walk_partial(alg, cplx, m, n, a, lda, 0, k0, k1, 0, c->part[i], 1, c->streams[i]);
+  }
+  if (st) {
+    cudaSetDevice(cur);
+    return st;
+  }
+  NcclApi& api = nccl_api();
+  ncclResult_t r = api.groupStart();
+  for (int i = 0; i < ngpu && r == ncclSuccess; ++i)
+    r = api.allGather(c->part[i], c->gathered[i], 8, ncclFloat64, c->comms[i], c->streams[i]);
+  const ncclResult_t r2 = api.groupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess) {
+    cudaSetDevice(cur);
+    return nccl_fail(r != ncclSuccess ? r : r2, "ncclAllGather");
+  }
+  PERM_CUDA_TRY(cudaSetDevice(devs[0]));
+  PERM_CUDA_TRY(cudaMemcpyAsync(parts, c->gathered[0], (size_t)ngpu * 8 * sizeof(double), cudaMemcpyDeviceToHost,
+                                c->streams[0]));
+  for (int i = 0; i < ngpu; ++i) {
+    PERM_CUDA_TRY(cudaSetDevice(devs[i]));
+    PERM_CUDA_TRY(cudaStreamSynchronize(c->streams[i]));
+  }
+  PERM_CUDA_TRY(cudaSetDevice(cur));
+  return PERM_OK;
+}
+
+// Exchange for perm_sharded_{f64,c128}: NCCL when the devices are distinct
+// and libnccl is present, else the host-worker path.  PERM_SHARDED_EXCHANGE
+// = "nccl" / "host" forces one.
+bool use_nccl_exchange(int ngpu, const int* devices) {
+  const char* e = std::getenv("PERM_SHARDED_EXCHANGE");
+  const std::string mode = e ? e : "";
+  if (mode == "host") return false;
+  std::vector<int> d(devices, devices + ngpu);
+  std::sort(d.begin(), d.end());
+  if (std::adjacent_find(d.begin(), d.end()) != d.end()) return false;  // a device listed twice
+  if (mode != "nccl" && ngpu < 2) return false;
+  return nccl_api().ok;
+}
+
 int sharded_float(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int ngpu, const int* devices,
                   double* out, double* magsum) {
   clear_error();
@@ -278,6 +419,11 @@ int sharded_float(int alg, bool cplx, int m, int n, const double* a, int64_t lda
     return PERM_BAD_ARG;
   }
   std::vector<double> parts((size_t)std::max(ngpu, 1) * 8, 0.0);
+  if (ngpu >= 1 && ngpu <= 64 && devices && magsum == nullptr && use_nccl_exchange(ngpu, devices)) {
+    st = sharded_float_nccl(alg, cplx, m, n, a, lda, ngpu, devices, parts.data());
+    if (st) return st;
+    return walk_finish(alg, cplx, m, n, a, lda, parts.data(), ngpu, out, magsum);
+  }
   st = run_shards(alg, m, n, ngpu, devices, [&](int i, uint64_t k0, uint64_t k1) {
     return walk_partial(alg, cplx, m, n, a, lda, 0, k0, k1, magsum != nullptr, &parts[(size_t)i * 8], 0, nullptr);
   });
@@ -461,6 +607,11 @@ int perm_walk_partial_i64(int alg, int m, int n, const int64_t* a, int64_t lda, 
 int perm_walk_finish_i64(int alg, int m, int n, const int64_t* a, int64_t lda, int width, const int64_t* partials,
                          int G, int64_t* out, int* fits_int64) {
   return int_walk_finish(alg, m, n, a, lda, width, partials, G, out, fits_int64);
+}
+
+int perm_sharded_exchange(int ngpu, const int* devices) {
+  if (ngpu < 1 || ngpu > 64 || devices == nullptr) return -1;
+  return use_nccl_exchange(ngpu, devices) ? 1 : 0;
 }
 
 int perm_sharded_f64(int alg, int m, int n, const double* a, int64_t lda, int ngpu, const int* devices, double* out,

@@ -101,6 +101,29 @@ def test_multi_device_driver():
         P.multi_device_permanent(a, devices=())
 
 
+def test_multi_device_driver_nccl_exchange(monkeypatch):
+    """perm_sharded_* with the NCCL exchange (ncclCommInitAll over the device
+    list + one grouped ncclAllGather of the 8-double partials), forced on a
+    single-device list here; results identical to the host exchange."""
+    a = W.c5(24)
+    monkeypatch.setenv("PERM_SHARDED_EXCHANGE", "host")
+    host = P.multi_device_permanent(a, devices=(0,))
+    monkeypatch.setenv("PERM_SHARDED_EXCHANGE", "nccl")
+    import ctypes as C
+
+    from paper_2510_03421_b200 import _lib
+
+    assert _lib.load().perm_sharded_exchange(1, (C.c_int * 1)(0)) == 1  # libnccl loaded: NCCL path
+    assert _lib.load().perm_sharded_exchange(2, (C.c_int * 2)(0, 0)) == 0  # duplicate device: host path
+    for _ in range(2):  # second call reuses the cached communicator
+        assert P.multi_device_permanent(a, devices=(0,)) == host
+    c = W.c3b()[:14, :20]
+    nccl = P.multi_device_permanent(c, devices=(0,))
+    monkeypatch.setenv("PERM_SHARDED_EXCHANGE", "host")
+    assert P.multi_device_permanent(c, devices=(0,)) == nccl
+    assert P.multi_device_permanent(c, devices=(0, 0)) == pytest.approx(nccl, rel=1e-12)
+
+
 def test_sharded_nccl_single_rank_int():
     import os
     import socket
