@@ -34,7 +34,10 @@
 
 namespace permb200 {
 
-constexpr int kWalkThreads = 256;
+#ifndef WALK_THREADS
+#define WALK_THREADS 256
+#endif
+constexpr int kWalkThreads = WALK_THREADS;
 constexpr int kWalkWarps = kWalkThreads / 32;
 constexpr int kPartialStride = 8;  // doubles per block partial: hi, lo, im_hi, im_lo, mag, -, -, -
 
@@ -263,7 +266,7 @@ __host__ __device__ constexpr int walk_min_blocks() {
 #ifdef WALK_MINB
   return WALK_MINB;
 #endif
-  return (Num<T>::kDoubles == 1) ? ((P <= 20) ? 3 : (P <= 44) ? 2 : 1) : ((P <= 14) ? 2 : 1);
+  return (Num<T>::kDoubles == 1) ? ((P <= 20) ? 3 : (P <= 41) ? 2 : 1) : ((P <= 14) ? 2 : 1);
 }
 
 template <typename T, int P, bool W, bool MAG>
