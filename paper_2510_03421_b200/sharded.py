@@ -234,3 +234,51 @@ def multi_device_permanent(a, alg: str = "glynn", devices=(0,), mag: bool = Fals
                   C.byref(mg) if mag else None), "sharded")
     value = complex(out[0], out[1]) if cplx else float(out[0])
     return (value, mg.value) if mag else value
+
+
+def batch_slice(B: int, rank: int, world: int):
+    """Contiguous slice [b0, b1) of a batch of B matrices for `rank`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return B * rank // world, B * (rank + 1) // world
+
+
+def sharded_batch(a, alg=None, group=None, batch_fn=None):
+    """A [B, m, n] float64 / complex128 batch split over the ranks of
+    ``group`` (matrices are independent, no collective but the
+    gather of the 8- or 16-byte results).  Rank r evaluates its contiguous
+    slice with the batch kernels (``alg`` as in ``opt_batch``: None = batch
+    dispatch, or "glynn" / "ryser" / "combinatoric"); one all-gather returns
+    the whole [B] result on every rank, in batch order.  ``batch_fn`` lets
+    tests substitute a CPU evaluator (gloo, no device)."""
+    import torch
+    import torch.distributed as dist
+
+    from .batch import _run
+
+    arr = np.asarray(a)
+    if arr.ndim != 3:
+        raise TypeError(f"expected a [B, m, n] array, got ndim={arr.ndim}")
+    cplx = np.iscomplexobj(arr)
+    rank, world, backend = _world(group)
+    B = arr.shape[0]
+    b0, b1 = batch_slice(B, rank, world)
+    part = arr[b0:b1]
+    vals = np.asarray(batch_fn(part) if batch_fn is not None else _run(part, alg),
+                      dtype=np.complex128 if cplx else np.float64)
+    if world == 1:
+        return vals
+    # equal-size slots for all_gather_into_tensor: pad every slice to the
+    # largest, as real doubles (complex -> 2 doubles per matrix)
+    w = 2 if cplx else 1
+    slot = -(-B // world)
+    buf = np.zeros(slot * w)
+    buf[: (b1 - b0) * w] = vals.view(np.float64)
+    dev = "cuda" if backend == "nccl" else "cpu"
+    t = torch.from_numpy(buf).to(dev)
+    gathered = torch.empty(world * slot * w, dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(gathered, t, group=group)
+    g = gathered.cpu().numpy().reshape(world, slot * w)
+    out = np.concatenate([g[r, : (batch_slice(B, r, world)[1] - batch_slice(B, r, world)[0]) * w]
+                          for r in range(world)])
+    return out.view(np.complex128) if cplx else out

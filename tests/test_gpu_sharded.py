@@ -141,5 +141,7 @@ def test_sharded_nccl_single_rank_int():
         assert P.sharded_permanent(W.c4b(), exact="int128") == int(c4["c4b_exact"])
         small = np.random.default_rng(4).integers(0, 3, (11, 11)).astype(np.int64)
         assert P.sharded_permanent(small, alg="ryser") == O.exact_int128("ryser", small)
+        A = W.c1()
+        np.testing.assert_array_equal(P.sharded_batch(A), P.opt_batch(A))
     finally:
         dist.destroy_process_group()
