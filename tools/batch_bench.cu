@@ -4,6 +4,12 @@
 #include <vector>
 #include "../paper_2510_03421_b200/csrc/batch.cuh"
 using namespace permb200;
+// experiment: no shared-memory staging, each thread reads its matrix through L1
+template <typename T, int N, int TPB>
+__global__ void __launch_bounds__(TPB) glynn_l1_kernel(const T* __restrict__ a, T* __restrict__ out, int64_t nb) {
+  const int64_t i = (int64_t)blockIdx.x * TPB + threadIdx.x;
+  if (i < nb) out[i] = Num<T>::scale(1.0 / (double)(1 << (N - 1)), batch_glynn_one<T, N>(a + i * N * N));
+}
 template <typename K>
 float timeit(K launch, int reps) {
   launch();
@@ -28,6 +34,13 @@ int main() {
     cudaFuncSetAttribute(batch_glynn_kernel<double, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     float ms = timeit([&] { batch_glynn_kernel<double, 8><<<(B + kBatchThreads - 1) / kBatchThreads, kBatchThreads, smem>>>(a, out, B); }, 10);
     printf("threads=%d glynn 8x8 1e6: %.4f ms  %.2f Tops  err=%s\n", kBatchThreads, ms, B * 2048.0 / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+  }
+  {
+    float ms32 = timeit([&] { glynn_l1_kernel<double, 8, 32><<<(B + 31) / 32, 32>>>(a, out, B); }, 10);
+    float ms64 = timeit([&] { glynn_l1_kernel<double, 8, 64><<<(B + 63) / 64, 64>>>(a, out, B); }, 10);
+    float ms128 = timeit([&] { glynn_l1_kernel<double, 8, 128><<<(B + 127) / 128, 128>>>(a, out, B); }, 10);
+    printf("L1-direct glynn 8x8 1e6: tpb32 %.4f ms, tpb64 %.4f ms, tpb128 %.4f ms err=%s\n", ms32, ms64, ms128,
+           cudaGetErrorString(cudaGetLastError()));
   }
   {
     constexpr int STRIDE = 40 | 1;
