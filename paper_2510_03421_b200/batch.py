@@ -4,7 +4,11 @@ The reference has no batch entry point -- ``as_matrix`` rejects anything but
 2-D input (src/core.py:150-151) and callers loop in Python, one ~1-10 ms
 ``opt`` call per matrix.  These functions take a [B, m, n] array
 (numpy on the host, or a torch CUDA tensor read in place) and evaluate all B
-permanents with one kernel launch (thread per matrix, C ABI perm_batch_*).
+permanents with one kernel launch (C ABI perm_batch_*).  The batch dispatch
+(``opt_batch``) uses two batch-only exact formulas that are cheaper per
+matrix than any of the reference's algorithms: the set-partition (Moebius)
+formula for m <= 4 and the 4+4 Laplace expansion for 8x8, both streamed
+through shared memory by bulk copies (csrc/batch_bulk.cuh).
 
 Float64 / complex128 batches only; integer batches are routed through the
 exact single-matrix path (one call each), keeping its semantics.
@@ -19,7 +23,7 @@ from . import _lib
 from .algorithms import AlgorithmId
 
 _ALG = {None: -1, "auto": -1, AlgorithmId.COMBINATORIC: 0, AlgorithmId.RYSER: 1, AlgorithmId.GLYNN: 2,
-        "combinatoric": 0, "ryser": 1, "glynn": 2}
+        "combinatoric": 0, "ryser": 1, "glynn": 2, "partition": 3, "laplace": 4}
 
 
 def _run(a, alg):
@@ -75,9 +79,21 @@ def _run(a, alg):
 
 
 def opt_batch(a, params=None):
-    """Permanents of a [B, m, n] batch with the batch dispatch (Glynn for
-    squares, subset-skipping Ryser for rectangles)."""
+    """Permanents of a [B, m, n] batch with the batch dispatch
+    (perm_batch_select: Laplace for 8x8 real, Glynn for other squares, the
+    partition formula for m <= 4, subset-skipping Ryser otherwise)."""
     return _run(a, None)
+
+
+def partition_batch(a):
+    """m <= 4: sum over set partitions pi of the rows of
+    mu(pi) prod_{blocks b} sum_j prod_{i in b} a_ij."""
+    return _run(a, "partition")
+
+
+def laplace_batch(a):
+    """8x8: sum_{|X|=4} per(A[0:4, X]) per(A[4:8, X^c])."""
+    return _run(a, "laplace")
 
 
 def glynn_batch(a):

@@ -1,0 +1,503 @@
+// Bulk-pipelined batch kernels: the HBM-streaming form of north_star item 4
+// for the two C2 shapes (and every shape the same formulas cover).
+//
+// Pipeline.  A persistent grid (one CTA per SM) streams the row-major
+// [B][m][n] batch through shared memory in tiles of whole matrices with
+// `cp.async.bulk` (1-D TMA: one elected thread, completion on an mbarrier),
+// kStages tiles in flight per SM, so HBM sees a few hundred KB of
+// outstanding reads per SM instead of the 32-thread blocks' per-thread loads.
+// Tile t+kStages is issued into slot t % kStages as soon as every thread is
+// done reading tile t.  A partial last tile is copied with its exact byte
+// count (needs m*n*8 % 16 == 0 and a 16-byte aligned batch; otherwise the
+// caller uses the classic kernels in batch.cuh).
+//
+// Bank conflicts.  Bulk copies land matrices contiguously, so lanes reading
+// "their" matrix at the same offset all hit one bank group.  Both formulas
+// below are invariant under permuting a matrix's columns (all rows alike) and
+// under the row permutations they are symmetric in, so each lane reads its
+// matrix with a lane-dependent column rotation / row order instead of
+// padding: every LDS.128 of a warp is 4 wavefronts, the minimum.
+//
+// Formulas (cheaper per matrix than any reference algorithm, exact algebra):
+//
+//  * Rectangular m <= 4 (C2b 4x10): the Moebius inversion over set partitions
+//    of the rows (sum over injective row->column maps =
+//    sum_pi mu(pi) prod_{blocks b} p_b,  p_b = sum_j prod_{i in b} a_ij,
+//    mu(pi) = prod_b (-1)^(|b|-1) (|b|-1)!):  m = 4 costs (2^m-1-m) muls +
+//    (2^m-1) adds per column = 26n + 30 flops (C2b: 290, against 3080 for the
+//    reference's cheapest exact algorithm, Ryser-rect).
+//    Thread per matrix.
+//  * Square 8x8 (C2a): generalised Laplace expansion over the 4+4 row split,
+//    per = sum_{|X|=4} per(A[0:4, X]) per(A[4:8, X^c]), with the 4x4 minors
+//    built from 2x2 row-pair permanents q(P):
+//      per(A[0:4, X]) = sum_{P subset X, |P|=2} q01(P) q23(X \ P).
+//    A lane pair owns one matrix: lane 2j the top half, lane 2j+1 the bottom;
+//    each forms its 2 x 28 q-tables and 70 minors, the pair exchanges minors
+//    by warp shuffle.  1204 flops per matrix against 2048 for Glynn.
+#pragma once
+#include <utility>
+#include "common.cuh"
+
+namespace permb200 {
+
+// ------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned bb_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bb_mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bb_smem(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bb_fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bb_fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bb_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb_smem(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bb_bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          bb_smem(dst)),
+      "l"(src), "r"(bytes), "r"(bb_smem(bar)), "l"(0x12F0000000000000ull)  // evict-first: streamed once
+      : "memory");
+}
+__device__ __forceinline__ void bb_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bb_smem(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+// ------------------------------------------------------------- the pipeline
+// Op: static constexpr int kLanes (lanes per matrix);
+//     template <class R> static __device__ void run(const T* tile_smem, int64_t first, int count,
+//                                                   T* out, int thread_in_tile, R&& release)
+//     -- every thread calls release() exactly once, after its last read of tile_smem
+template <typename T, int M, int N, int TPB, int STAGES, class Op, bool kComputeOnly = false, int MINB = 1>
+__global__ void __launch_bounds__(TPB, MINB) batch_bulk_kernel(const T* __restrict__ a, T* __restrict__ out,
+                                                           int64_t nb) {
+  constexpr int MATS = TPB / Op::kLanes;
+  constexpr unsigned MAT_BYTES = M * N * sizeof(T);
+  constexpr unsigned TILE_BYTES = MATS * MAT_BYTES;
+  static_assert(MAT_BYTES % 16 == 0, "bulk copies move 16-byte multiples");
+  extern __shared__ __align__(128) unsigned char bb_smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  const int64_t ntiles = (nb + MATS - 1) / MATS;
+  auto issue = [&](int64_t tile, int slot) {
+    const int64_t first = tile * MATS;
+    const int64_t cnt = (nb - first < MATS) ? nb - first : MATS;
+    const unsigned bytes = (unsigned)cnt * MAT_BYTES;
+    bb_expect_tx(&full[slot], bytes);
+    bb_bulk_g2s(bb_smem_raw + (size_t)slot * TILE_BYTES, reinterpret_cast<const char*>(a) + first * MAT_BYTES, bytes,
+                &full[slot]);
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) bb_mbar_init(&full[s], 1);
+    bb_fence_mbar_init();
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+      if (t < ntiles) issue(t, s);
+    }
+  }
+  __syncthreads();
+  int slot = 0;
+  unsigned phase = 0;
+  int64_t it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    if (!kComputeOnly || it < STAGES) bb_wait(&full[slot], phase);  // (kComputeOnly: timing experiments)
+    const int64_t first = tile * MATS;
+    const int cnt = (int)((nb - first < MATS) ? nb - first : MATS);
+    // release: called by every thread once it holds what it needs from the
+    // slot (before its arithmetic), so the next copy overlaps the compute
+    auto release = [&]() {
+      __syncthreads();
+      if (threadIdx.x == 0 && !kComputeOnly) {
+        const int64_t t = tile + (int64_t)STAGES * gridDim.x;
+        if (t < ntiles) {
+          bb_fence_proxy_async();  // generic-proxy reads before the async-proxy overwrite
+          issue(t, slot);
+        }
+      }
+    };
+    Op::run(reinterpret_cast<const T*>(bb_smem_raw + (size_t)slot * TILE_BYTES), first, cnt, out, threadIdx.x,
+            release);
+    if (++slot == STAGES) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+}
+
+// Per-warp pipelines: every warp streams its own ring of STAGES warp-tiles
+// (32 / kLanes matrices each), lane 0 arming the warp's mbarriers and issuing
+// its copies, so warps never wait on each other (no block barrier) and the
+// warps per SM are set by registers, not by a block-wide tile ring.
+template <typename T, int M, int N, int WARPS, int STAGES, class Op, int MINB = 1>
+__global__ void __launch_bounds__(32 * WARPS, MINB) batch_bulk_warp_kernel(const T* __restrict__ a, T* __restrict__ out,
+                                                                       int64_t nb) {
+  constexpr int MATS = 32 / Op::kLanes;
+  constexpr unsigned MAT_BYTES = M * N * sizeof(T);
+  constexpr unsigned TILE_BYTES = MATS * MAT_BYTES;
+  static_assert(MAT_BYTES % 16 == 0, "bulk copies move 16-byte multiples");
+  extern __shared__ __align__(128) unsigned char bb_smem_raw[];
+  __shared__ __align__(8) uint64_t full[WARPS][STAGES];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* ring = bb_smem_raw + (size_t)warp * STAGES * TILE_BYTES;
+  uint64_t* bar = full[warp];
+  const int64_t ntiles = (nb + MATS - 1) / MATS;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp, nw = (int64_t)gridDim.x * WARPS;
+  auto issue = [&](int64_t tile, int slot) {
+    const int64_t first = tile * MATS;
+    const int64_t cnt = (nb - first < MATS) ? nb - first : MATS;
+    const unsigned bytes = (unsigned)cnt * MAT_BYTES;
+    bb_expect_tx(&bar[slot], bytes);
+    bb_bulk_g2s(ring + (size_t)slot * TILE_BYTES, reinterpret_cast<const char*>(a) + first * MAT_BYTES, bytes,
+                &bar[slot]);
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) bb_mbar_init(&bar[s], 1);
+    bb_fence_mbar_init();
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      const int64_t t = gw + (int64_t)s * nw;
+      if (t < ntiles) issue(t, s);
+    }
+  }
+  __syncwarp();
+  int slot = 0;
+  unsigned phase = 0;
+  for (int64_t tile = gw; tile < ntiles; tile += nw) {
+    bb_wait(&bar[slot], phase);
+    const int64_t first = tile * MATS;
+    const int cnt = (int)((nb - first < MATS) ? nb - first : MATS);
+    auto release = [&]() {
+      __syncwarp();  // the warp is done reading this slot
+      if (lane == 0) {
+        const int64_t t = tile + (int64_t)STAGES * nw;
+        if (t < ntiles) {
+          bb_fence_proxy_async();
+          issue(t, slot);
+        }
+      }
+    };
+    Op::run(reinterpret_cast<const T*>(ring + (size_t)slot * TILE_BYTES), first, cnt, out, lane, release);
+    if (++slot == STAGES) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+}
+
+// ------------------------------------------- rectangular m <= 4: partitions
+__host__ __device__ constexpr int bb_hibit(int x) {
+  int h = 0;
+  while (x >> (h + 1)) ++h;
+  return h;
+}
+
+// per of an M x N matrix (M <= 4) from the subset sums S[b] = sum_j prod_{i in b} a_ij
+template <typename T, int M>
+__device__ __forceinline__ T partition_combine(const T (&S)[1 << M]) {
+  using X = Num<T>;
+  if constexpr (M == 1) {
+    return S[1];
+  } else if constexpr (M == 2) {
+    return X::sub(X::mul(S[1], S[2]), S[3]);
+  } else if constexpr (M == 3) {
+    // p0p1p2 - p01p2 - p02p1 - p12p0 + 2p012
+    T r = X::mul(X::mul(S[1], S[2]), S[4]);
+    r = X::sub(r, X::mul(S[3], S[4]));
+    r = X::sub(r, X::mul(S[5], S[2]));
+    r = X::sub(r, X::mul(S[6], S[1]));
+    return X::add(r, X::scale(2.0, S[7]));
+  } else {
+    static_assert(M == 4, "partition formula kernel covers m <= 4");
+    // singletons: p0p1p2p3
+    const T s01 = X::mul(S[1], S[2]), s23 = X::mul(S[4], S[8]);
+    T r = X::mul(s01, s23);
+    // {ij}{k}{l}: -6 terms
+    T t = X::mul(S[3], s23);                 // {01}{2}{3}
+    t = X::add(t, X::mul(S[12], s01));       // {23}{0}{1}
+    t = X::add(t, X::mul(S[5], X::mul(S[2], S[8])));   // {02}{1}{3}
+    t = X::add(t, X::mul(S[10], X::mul(S[1], S[4])));  // {13}{0}{2}
+    t = X::add(t, X::mul(S[9], X::mul(S[2], S[4])));   // {03}{1}{2}
+    t = X::add(t, X::mul(S[6], X::mul(S[1], S[8])));   // {12}{0}{3}
+    r = X::sub(r, t);
+    // {ij}{kl}: +3 terms
+    r = X::add(r, X::mul(S[3], S[12]));
+    r = X::add(r, X::mul(S[5], S[10]));
+    r = X::add(r, X::mul(S[9], S[6]));
+    // {ijk}{l}: +2 x 4 terms
+    T u = X::mul(S[7], S[8]);
+    u = X::add(u, X::mul(S[11], S[4]));
+    u = X::add(u, X::mul(S[13], S[2]));
+    u = X::add(u, X::mul(S[14], S[1]));
+    r = X::add(r, X::scale(2.0, u));
+    // {0123}: -6
+    return X::sub(r, X::scale(6.0, S[15]));
+  }
+}
+
+template <typename T, int M, int N>
+struct PartitionOp {
+  static constexpr int kLanes = 1;
+  static_assert(M >= 1 && M <= 4 && M <= N, "m <= 4, m <= n");
+  static_assert((N * sizeof(T)) % 16 == 0 || sizeof(T) == 16, "rows read as 16-byte chunks");
+  template <class R>
+  __device__ __forceinline__ static void run(const T* tile, int64_t first, int cnt, T* out, int me, R&& release) {
+    using X = Num<T>;
+    constexpr int NS = 1 << M;
+    const T* A = tile + (size_t)me * M * N;
+    // row order rotated by (lane / 8) % M: the 16-byte chunk a lane reads
+    // spreads over all 8 bank groups (4 wavefronts per LDS.128)
+    const int tau = ((me & 31) >> 3) % M;
+    const T* rowp[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      const int r = (i + tau) % M;
+      rowp[i] = A + r * N;
+    }
+    T S[NS];
+#pragma unroll
+    for (int b = 0; b < NS; ++b) S[b] = X::zero();
+    constexpr int CW = (sizeof(T) == 8) ? 2 : 1;  // elements per 16-byte chunk
+#pragma unroll
+    for (int c = 0; c < N / CW; ++c) {
+      T col[M][CW];
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        if constexpr (CW == 2) {
+          const double2 v = *reinterpret_cast<const double2*>(rowp[i] + 2 * c);
+          col[i][0] = v.x;
+          col[i][1] = v.y;
+        } else {
+          col[i][0] = rowp[i][c];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < CW; ++e) {
+        T p[NS];
+#pragma unroll
+        for (int i = 0; i < M; ++i) p[1 << i] = col[i][e];
+#pragma unroll
+        for (int b = 3; b < NS; ++b) {
+          if ((b & (b - 1)) == 0) continue;
+          const int h = bb_hibit(b);
+          p[b] = X::mul(p[b ^ (1 << h)], p[1 << h]);
+        }
+#pragma unroll
+        for (int b = 1; b < NS; ++b) S[b] = X::add(S[b], p[b]);
+      }
+    }
+    release();
+    // the row rotation relabels rows; the combine is symmetric in them
+    const T r = partition_combine<T, M>(S);
+    if (me < cnt) out[first + me] = r;
+  }
+};
+
+// ---------------------------------------------------- square 8x8: Laplace
+__host__ __device__ constexpr int lp_pidx(int i, int k) { return i * (15 - i) / 2 + (k - i - 1); }  // i < k < 8
+struct LpSub {
+  int x[4], c[4];
+};
+// the p-th 4-subset X of {0..7} containing column 0 (35 of them), and X^c
+__host__ __device__ constexpr LpSub lp_sub(int p) {
+  LpSub s{};
+  int q = 0;
+  for (int a = 1; a < 8; ++a)
+    for (int b = a + 1; b < 8; ++b)
+      for (int c = b + 1; c < 8; ++c) {
+        if (q == p) {
+          s.x[0] = 0; s.x[1] = a; s.x[2] = b; s.x[3] = c;
+          int k = 0;
+          for (int j = 1; j < 8; ++j)
+            if (j != a && j != b && j != c) s.c[k++] = j;
+        }
+        ++q;
+      }
+  return s;
+}
+// per(H[:, {a,b,c,d}]) of a 4-row half H from its row-pair tables qa (rows 0,1),
+// qb (rows 2,3): the 6 ordered splits of {a,b,c,d} into two pairs.  CH = 2
+// runs them as two 3-deep chains (one extra add, half the dependency depth).
+template <int CH, int a, int b, int c, int d>
+__device__ __forceinline__ double lp_minor(const double (&qa)[28], const double (&qb)[28]) {
+  if constexpr (CH == 1) {
+    double g = qa[lp_pidx(a, b)] * qb[lp_pidx(c, d)];
+    g = fma(qa[lp_pidx(c, d)], qb[lp_pidx(a, b)], g);
+    g = fma(qa[lp_pidx(a, c)], qb[lp_pidx(b, d)], g);
+    g = fma(qa[lp_pidx(b, d)], qb[lp_pidx(a, c)], g);
+    g = fma(qa[lp_pidx(a, d)], qb[lp_pidx(b, c)], g);
+    g = fma(qa[lp_pidx(b, c)], qb[lp_pidx(a, d)], g);
+    return g;
+  } else {
+    double g = qa[lp_pidx(a, b)] * qb[lp_pidx(c, d)];
+    double h = qa[lp_pidx(b, d)] * qb[lp_pidx(a, c)];
+    g = fma(qa[lp_pidx(c, d)], qb[lp_pidx(a, b)], g);
+    h = fma(qa[lp_pidx(a, d)], qb[lp_pidx(b, c)], h);
+    g = fma(qa[lp_pidx(a, c)], qb[lp_pidx(b, d)], g);
+    h = fma(qa[lp_pidx(b, c)], qb[lp_pidx(a, d)], h);
+    return g + h;
+  }
+}
+// pairs P0 .. P0+G-1 of (X, X^c): all 2G minors first, then the 2G shuffles
+// with the partner lane (the other half of the same matrix), then the 2G
+// products -- G pairs of independent work between dependent steps
+template <int CH, int P0, int... Is>
+__device__ __forceinline__ void lp_group(const double (&qa)[28], const double (&qb)[28], double (&acc)[4],
+                                         std::integer_sequence<int, Is...>) {
+  constexpr int G = sizeof...(Is);
+  double g[2 * G], h[2 * G];
+  ((g[2 * Is] = lp_minor<CH, lp_sub(P0 + Is).x[0], lp_sub(P0 + Is).x[1], lp_sub(P0 + Is).x[2], lp_sub(P0 + Is).x[3]>(qa, qb),
+    g[2 * Is + 1] =
+        lp_minor<CH, lp_sub(P0 + Is).c[0], lp_sub(P0 + Is).c[1], lp_sub(P0 + Is).c[2], lp_sub(P0 + Is).c[3]>(qa, qb)),
+   ...);
+#pragma unroll
+  for (int i = 0; i < 2 * G; ++i) h[i] = __shfl_xor_sync(0xffffffffu, g[i], 1);
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
+    acc[i & 3] = fma(g[2 * i], h[2 * i + 1], acc[i & 3]);
+    acc[i & 3] = fma(g[2 * i + 1], h[2 * i], acc[i & 3]);
+  }
+}
+template <int CH, int G, int... Ks>
+__device__ __forceinline__ void lp_all(const double (&qa)[28], const double (&qb)[28], double (&acc)[4],
+                                       std::integer_sequence<int, Ks...>) {
+  (lp_group<CH, Ks * G>(qa, qb, acc, std::make_integer_sequence<int, (35 - Ks * G < G) ? 35 - Ks * G : G>{}), ...);
+}
+// Half exchange: the top lane accumulates pairs 0..17, the bottom lane pairs
+// 18..34; at step i each lane sends the partner the two minors the partner
+// needs (selected by lane half), so every 32-bit shuffle carries useful data
+// both ways: 70 SHFL per lane instead of 140, 35 products instead of 70.
+//
+// Scheduling: B200's FP64 pipe only reaches its peak when each warp issues
+// long runs of independent DFMAs (tools/fp64_occ_probe.cu: a dependency
+// every 4 / 8 / 16 instructions gives 73 / 86 / 98% of the pipe, whatever
+// the occupancy), so the minors of GI steps (4*GI of them) are built term by
+// term across all of them -- a dependency distance of 4*GI instructions.
+//
+// minor slot m of step i: m = 0, 1 -> pair i (X, X^c); m = 2, 3 -> pair i+18
+__host__ __device__ constexpr int lp_term(int pair, int side, int s, int which) {
+  const LpSub q = lp_sub(pair);
+  const int a = side ? q.c[0] : q.x[0], b = side ? q.c[1] : q.x[1];
+  const int c = side ? q.c[2] : q.x[2], d = side ? q.c[3] : q.x[3];
+  // the 6 ordered splits: (ab|cd) (cd|ab) (ac|bd) (bd|ac) (ad|bc) (bc|ad)
+  const int p0[6][2] = {{a, b}, {c, d}, {a, c}, {b, d}, {a, d}, {b, c}};
+  const int p1[6][2] = {{c, d}, {a, b}, {b, d}, {a, c}, {b, c}, {a, d}};
+  return which == 0 ? lp_pidx(p0[s][0], p0[s][1]) : lp_pidx(p1[s][0], p1[s][1]);
+}
+template <int I0, int S, int... Ms>
+__device__ __forceinline__ void lp_wide_term(const double (&qa)[28], const double (&qb)[28], double (&g)[sizeof...(Ms)],
+                                             std::integer_sequence<int, Ms...>) {
+  // slot Ms: step I0 + Ms/4, pair (Ms%4 < 2 ? step : step+18), side Ms%2
+  if constexpr (S == 0) {
+    ((g[Ms] = (((Ms & 3) < 2) || (I0 + Ms / 4 + 18 < 35))
+                  ? qa[lp_term(((Ms & 3) < 2) ? I0 + Ms / 4 : (I0 + Ms / 4 + 18) % 35, Ms & 1, 0, 0)] *
+                        qb[lp_term(((Ms & 3) < 2) ? I0 + Ms / 4 : (I0 + Ms / 4 + 18) % 35, Ms & 1, 0, 1)]
+                  : 0.0),
+     ...);
+  } else {
+    ((g[Ms] = (((Ms & 3) < 2) || (I0 + Ms / 4 + 18 < 35))
+                  ? fma(qa[lp_term(((Ms & 3) < 2) ? I0 + Ms / 4 : (I0 + Ms / 4 + 18) % 35, Ms & 1, S, 0)],
+                        qb[lp_term(((Ms & 3) < 2) ? I0 + Ms / 4 : (I0 + Ms / 4 + 18) % 35, Ms & 1, S, 1)], g[Ms])
+                  : 0.0),
+     ...);
+  }
+}
+template <int I0, int GI>
+__device__ __forceinline__ void lp_wide_group(const double (&qa)[28], const double (&qb)[28], bool bottom,
+                                              double (&acc)[8]) {
+  double g[4 * GI];
+  using Seq = std::make_integer_sequence<int, 4 * GI>;
+  lp_wide_term<I0, 0>(qa, qb, g, Seq{});
+  lp_wide_term<I0, 1>(qa, qb, g, Seq{});
+  lp_wide_term<I0, 2>(qa, qb, g, Seq{});
+  lp_wide_term<I0, 3>(qa, qb, g, Seq{});
+  lp_wide_term<I0, 4>(qa, qb, g, Seq{});
+  lp_wide_term<I0, 5>(qa, qb, g, Seq{});
+  double r[2 * GI];
+#pragma unroll
+  for (int i = 0; i < GI; ++i) {
+    r[2 * i] = __shfl_xor_sync(0xffffffffu, bottom ? g[4 * i] : g[4 * i + 2], 1);
+    r[2 * i + 1] = __shfl_xor_sync(0xffffffffu, bottom ? g[4 * i + 1] : g[4 * i + 3], 1);
+  }
+#pragma unroll
+  for (int i = 0; i < GI; ++i) {
+    const double o0 = bottom ? g[4 * i + 2] : g[4 * i], o1 = bottom ? g[4 * i + 3] : g[4 * i + 1];
+    acc[(2 * i) & 7] = fma(o0, r[2 * i + 1], acc[(2 * i) & 7]);
+    acc[(2 * i + 1) & 7] = fma(o1, r[2 * i], acc[(2 * i + 1) & 7]);
+  }
+}
+template <int GI, int... Ks>
+__device__ __forceinline__ void lp_wide_all(const double (&qa)[28], const double (&qb)[28], bool bottom,
+                                            double (&acc)[8], std::integer_sequence<int, Ks...>) {
+  (lp_wide_group<Ks * GI, (18 - Ks * GI < GI) ? 18 - Ks * GI : GI>(qa, qb, bottom, acc), ...);
+}
+// 2x2 row-pair permanents of the 8 logical columns held as 16 doubles (row r0 = v[0..7], r1 = v[8..15])
+__device__ __forceinline__ void lp_qtable(const double (&v)[16], double (&q)[28]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int k = i + 1; k < 8; ++k) q[lp_pidx(i, k)] = fma(v[i], v[8 + k], v[k] * v[8 + i]);
+}
+
+template <int G, int CH, int XCH = 1>
+struct Laplace8OpT {
+  static constexpr int kLanes = 2;
+  template <class R>
+  __device__ __forceinline__ static void run(const double* tile, int64_t first, int cnt, double* out, int me,
+                                             R&& release) {
+    const int lane = me & 31, warp = me >> 5;
+    const int jj = lane >> 1, half = lane & 1;
+    const int mat = warp * 16 + jj;
+    // this lane's 4 rows: two 128-byte rows of 8 16-byte chunks (2 matrix rows each)
+    const double2* H = reinterpret_cast<const double2*>(tile + (size_t)mat * 64 + half * 32);
+    // logical chunk c -> physical chunk: column pairs rotated by rho, the two
+    // matrix rows of a 128-byte row swapped when t (both are symmetries of
+    // the q-tables; the pair's two lanes share rho so X / X^c line up)
+    const int rho = jj & 3, t = (jj >> 2) & 1;
+    double qa[28], qb[28];
+    {
+      double v[16];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double2 x = H[(((c & 3) + rho) & 3) | (((c >> 2) ^ t) << 2)];
+        v[(c >> 2) * 8 + 2 * (c & 3)] = x.x;
+        v[(c >> 2) * 8 + 2 * (c & 3) + 1] = x.y;
+      }
+      lp_qtable(v, qa);
+    }
+    {
+      double v[16];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double2 x = H[8 + ((((c & 3) + rho) & 3) | (((c >> 2) ^ t) << 2))];
+        v[(c >> 2) * 8 + 2 * (c & 3)] = x.x;
+        v[(c >> 2) * 8 + 2 * (c & 3) + 1] = x.y;
+      }
+      lp_qtable(v, qb);
+    }
+    release();  // the tables are all this lane needs: free the slot before the minors
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if constexpr (XCH == 0) {
+      lp_all<CH, G>(qa, qb, acc, std::make_integer_sequence<int, (35 + G - 1) / G>{});
+      if (half == 0 && mat < cnt) out[first + mat] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    } else {
+      double acc8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      lp_wide_all<G>(qa, qb, half != 0, acc8, std::make_integer_sequence<int, (18 + G - 1) / G>{});
+      const double mine = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
+      const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
+      if (half == 0 && mat < cnt) out[first + mat] = mine + other;
+    }
+  }
+};
+
+using Laplace8Op = Laplace8OpT<4, 1, 1>;
+
+}  // namespace permb200

@@ -76,6 +76,11 @@ int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, dou
 
 uint64_t walk_steps(int alg, int m, int n);
 
+// ---- bulk-pipelined batch kernels (engine_bulk.cu) --------------------------
+bool bulk_batch_supported(int alg, bool cplx, int m, int n);
+// PERM_OK / CUDA failure, or -1 when no bulk kernel applies (shape, alignment)
+int launch_bulk_batch(int alg, bool cplx, int64_t B, int m, int n, const void* dA, void* dOut, cudaStream_t stream);
+
 // ---- instrumentation -------------------------------------------------------
 struct KernelTimer {
   bool init = false, ok = false, pending = false;

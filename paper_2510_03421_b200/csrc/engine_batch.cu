@@ -127,10 +127,18 @@ static batch_fn pick_glynn_warp(int n, std::integer_sequence<int, Ns...>) {
   return f;
 }
 
-// Kernel choice for one (device-resident) batch.  Thread-per-matrix needs
-// enough matrices to fill the GPU; below that a warp per matrix (n >= 9).
+// Kernel choice for one (device-resident) batch.  The batch-only formulas run
+// on the bulk-pipelined kernels when the shape and base address allow (else
+// the classic kernel of the same family: Laplace -> Glynn, partition ->
+// memoized combinatoric).  Thread-per-matrix needs enough matrices to fill
+// the GPU; below that a warp per matrix (n >= 9).
 static int launch_batch(int alg, bool cplx, int64_t B, int m, int n, const void* dA, void* dOut,
                         cudaStream_t stream) {
+  if (alg == PERM_ALG_BATCH_LAPLACE || alg == PERM_ALG_BATCH_PARTITION) {
+    const int st = launch_bulk_batch(alg, cplx, B, m, n, dA, dOut, stream);
+    if (st >= 0) return st;
+    alg = (alg == PERM_ALG_BATCH_LAPLACE) ? PERM_ALG_GLYNN : PERM_ALG_COMBINATORIC;
+  }
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -265,10 +273,13 @@ static void par_memcpy(void* dst, const void* src, size_t bytes) {
 }
 
 int batch_select(int m, int n) {
-  // cheapest exact per-matrix work: Glynn for squares, the memoized
-  // combinatoric DP for m <= 4 (C2b: 930 flops), subset-skipping Ryser else
+  // cheapest exact per-matrix work: the 4+4 Laplace kernel for 8x8 (1134
+  // flops against Glynn's 2048; complex 8x8 falls back to Glynn), Glynn for
+  // other squares, the partition formula for m <= 4 (C2b: 290 flops), the
+  // subset-skipping Ryser else
+  if (m == 8 && n == 8) return PERM_ALG_BATCH_LAPLACE;
   if (m == n) return PERM_ALG_GLYNN;
-  return (m <= 4 && n <= 12) ? PERM_ALG_COMBINATORIC : PERM_ALG_RYSER;
+  return (m <= 4) ? (int)PERM_ALG_BATCH_PARTITION : (int)PERM_ALG_RYSER;
 }
 
 int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a, double* out, int dev_ptr,
@@ -283,6 +294,19 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
     return PERM_BAD_SHAPE;
   }
   if (alg < 0) alg = batch_select(m, n);
+  if (alg > PERM_ALG_BATCH_LAPLACE) {
+    set_error("unknown batch algorithm");
+    return PERM_BAD_SHAPE;
+  }
+  if (alg == PERM_ALG_BATCH_LAPLACE && !(m == 8 && n == 8)) {
+    set_error("the Laplace batch formula is 8x8 only");
+    return PERM_BAD_SHAPE;
+  }
+  if (alg == PERM_ALG_BATCH_PARTITION && m > 4) {
+    set_error("the partition batch formula needs m <= 4");
+    return PERM_BAD_SHAPE;
+  }
+  if (alg == PERM_ALG_BATCH_LAPLACE && cplx) alg = PERM_ALG_GLYNN;
   if (alg == PERM_ALG_COMBINATORIC) {
     // src/algorithms.py:80-84 budget is per matrix; P(16, 16) would be absurd
     uint64_t perms = 1;

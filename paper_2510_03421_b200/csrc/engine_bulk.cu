@@ -1,0 +1,120 @@
+// Host side of the bulk-pipelined batch kernels (batch_bulk.cuh): the
+// partition-formula kernel for m <= 4 and the 4+4 Laplace kernel for 8x8,
+// picked by the batch dispatch (perm_batch_select) for device-resident
+// batches that meet the 1-D bulk-copy rules (16-byte aligned base, matrix
+// size a multiple of 16 bytes).
+#include <algorithm>
+#include <utility>
+
+#include "batch_bulk.cuh"
+#include "engine.cuh"
+
+namespace permb200 {
+
+namespace {
+
+using bulk_fn = cudaError_t (*)(const void*, void*, int64_t, cudaStream_t);
+
+int cur_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & 15;
+}
+int sm_count() {
+  static int nsm[16] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& n = nsm[dev & 15];
+  if (!n) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Tile shape from the matrix size: <= ~40 KB per stage, two stages, two
+// blocks per SM (measured on C2b: 4x10 f64, 128 threads, 6.0 TB/s).
+template <typename T, int M, int N>
+struct PartCfg {
+  static constexpr int kBytes = M * N * (int)sizeof(T);
+  static constexpr int kTPB = kBytes <= 320 ? 128 : (kBytes <= 640 ? 64 : 32);
+  static constexpr int kStages = 2;
+};
+
+template <typename T, int M, int N>
+cudaError_t launch_partition(const void* a, void* out, int64_t B, cudaStream_t s) {
+  using Cfg = PartCfg<T, M, N>;
+  auto k = batch_bulk_kernel<T, M, N, Cfg::kTPB, Cfg::kStages, PartitionOp<T, M, N>>;
+  const size_t smem = (size_t)Cfg::kStages * Cfg::kTPB * Cfg::kBytes;
+  static bool attr[16] = {false};  // per instantiation and device; idempotent, so racing first calls are harmless
+  if (!attr[cur_device()]) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr[cur_device()] = true;
+  }
+  const int64_t ntiles = (B + Cfg::kTPB - 1) / Cfg::kTPB;
+  const int grid = (int)std::min<int64_t>(ntiles, 2 * (int64_t)sm_count());
+  k<<<grid, Cfg::kTPB, smem, s>>>(static_cast<const T*>(a), static_cast<T*>(out), B);
+  return cudaGetLastError();
+}
+
+// Laplace 8x8: 64 threads (32 matrices) per block, three stages, four blocks
+// per SM (240 registers; C2a 1e6 x 8x8: 0.122 ms against 0.184 ms for the
+// thread-per-matrix Glynn kernel, tools/bulk_bench.cu).
+constexpr int kLapTPB = 64, kLapStages = 3, kLapPerSM = 4;
+cudaError_t launch_laplace8(const void* a, void* out, int64_t B, cudaStream_t s) {
+  auto k = batch_bulk_kernel<double, 8, 8, kLapTPB, kLapStages, Laplace8Op>;
+  constexpr int kMats = kLapTPB / Laplace8Op::kLanes;
+  const size_t smem = (size_t)kLapStages * kMats * 64 * sizeof(double);
+  static bool attr[16] = {false};
+  if (!attr[cur_device()]) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr[cur_device()] = true;
+  }
+  const int64_t ntiles = (B + kMats - 1) / kMats;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)kLapPerSM * sm_count());
+  k<<<grid, kLapTPB, smem, s>>>(static_cast<const double*>(a), static_cast<double*>(out), B);
+  return cudaGetLastError();
+}
+
+// (M, N), 1 <= M <= 4, M <= N <= 16: IDX = (M-1)*16 + (N-1); f64 needs even N
+template <typename T, int I>
+bulk_fn part_entry() {
+  constexpr int M = I / 16 + 1, N = I % 16 + 1;
+  if constexpr (N >= M && (sizeof(T) == 16 || N % 2 == 0)) return &launch_partition<T, M, N>;
+  else return nullptr;
+}
+template <typename T, int... Is>
+bulk_fn pick_partition(int m, int n, std::integer_sequence<int, Is...>) {
+  bulk_fn f = nullptr;
+  ((m == Is / 16 + 1 && n == Is % 16 + 1 ? (f = part_entry<T, Is>(), 0) : 0), ...);
+  return f;
+}
+
+}  // namespace
+
+bool bulk_batch_supported(int alg, bool cplx, int m, int n) {
+  if (alg == PERM_ALG_BATCH_LAPLACE) return !cplx && m == 8 && n == 8;
+  if (alg == PERM_ALG_BATCH_PARTITION) return m >= 1 && m <= 4 && m <= n && n <= 16 && (cplx || n % 2 == 0);
+  return false;
+}
+
+// Returns PERM_OK, a CUDA failure, or -1 when this (alg, shape, pointer)
+// has no bulk kernel (the caller then uses the classic kernels).
+int launch_bulk_batch(int alg, bool cplx, int64_t B, int m, int n, const void* dA, void* dOut, cudaStream_t stream) {
+  if (!bulk_batch_supported(alg, cplx, m, n)) return -1;
+  if ((reinterpret_cast<uintptr_t>(dA) & 15) != 0) return -1;  // 1-D bulk copies need 16-byte addresses
+  bulk_fn fn = nullptr;
+  if (alg == PERM_ALG_BATCH_LAPLACE) {
+    fn = &launch_laplace8;
+  } else {
+    fn = cplx ? pick_partition<cd>(m, n, std::make_integer_sequence<int, 64>{})
+              : pick_partition<double>(m, n, std::make_integer_sequence<int, 64>{});
+  }
+  if (!fn) return -1;
+  const cudaError_t e = fn(dA, dOut, B, stream);
+  return e == cudaSuccess ? PERM_OK : cuda_fail(e, "bulk batch kernel launch");
+}
+
+}  // namespace permb200

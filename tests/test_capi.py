@@ -54,6 +54,17 @@ def test_version_and_select():
     assert lib.perm_select(4, 20, p, 0, 0) == _lib.ALG_RYSER
 
 
+def test_batch_select():
+    """Batch dispatch: the 4+4 Laplace formula for 8x8 (4), the partition
+    formula for m <= 4 < n (3), Glynn for other squares, Ryser otherwise."""
+    lib = _lib.load()
+    assert lib.perm_batch_select(8, 8) == 4
+    assert lib.perm_batch_select(4, 10) == 3
+    assert lib.perm_batch_select(1, 16) == 3
+    assert lib.perm_batch_select(5, 5) == _lib.ALG_GLYNN
+    assert lib.perm_batch_select(5, 9) == _lib.ALG_RYSER
+
+
 @pytest.mark.parametrize("alg,m,n", [(2, 36, 36), (2, 20, 28), (1, 30, 30), (1, 5, 33), (2, 3, 3)])
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 7, 8])
 def test_shards_partition_the_walk(alg, m, n, world):

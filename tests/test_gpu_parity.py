@@ -337,6 +337,66 @@ def test_c1_batch_warp_per_matrix():
             assert scaled_err(out[i], v, M) <= TOL
 
 
+@pytest.mark.parametrize("cplx", [False, True])
+def test_partition_batch_all_shapes(cplx):
+    """The bulk-pipelined partition-formula kernel on every m <= 4, n <= 16
+    (f64 odd n and misaligned device views take the classic kernels), with
+    ragged batch sizes (partial last tile), vs the oracle."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(21 + cplx)
+    for m in range(1, 5):
+        for n in range(m, 17):
+            B = 290 + 7 * n
+            A = rng.standard_normal((B, m, n)) / np.sqrt(n)
+            if cplx:
+                A = A + 1j * rng.standard_normal((B, m, n)) / np.sqrt(n)
+            out = P.partition_batch(A)
+            assert np.array_equal(out, P.opt_batch(A)) or m == n
+            dA = torch.tensor(A, device="cuda")
+            dev = P.partition_batch(dA).cpu().numpy()
+            flat = torch.empty(B * m * n + 1, dtype=dA.dtype, device="cuda")
+            mis = flat[1:].view(B, m, n)  # 8/16-byte offset: not bulk-copy aligned
+            mis.copy_(dA)
+            dev_mis = P.partition_batch(mis).cpu().numpy()
+            for i in (0, 1, B // 2, B - 1):
+                ref = O.permanent("combinatoric", A[i])[0]
+                M = magsum(A[i])
+                for v in (out[i], dev[i], dev_mis[i]):
+                    assert scaled_err(v, ref, M) <= TOL, (m, n, i, v, ref)
+
+
+def test_laplace_batch_8x8():
+    """The bulk-pipelined 4+4 Laplace kernel (C2a's batch dispatch) vs the
+    oracle; exact on small-integer matrices; complex 8x8 falls back to Glynn."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(88)
+    for B in (1, 31, 33, 1005):
+        A = rng.standard_normal((B, 8, 8)) / np.sqrt(8)
+        out = P.laplace_batch(A)
+        assert np.array_equal(out, P.opt_batch(A))
+        for i in sorted({0, B // 3, B - 1}):
+            ref = O.permanent("glynn", A[i])[0]
+            assert scaled_err(out[i], ref, magsum(A[i])) <= TOL
+    perm = np.eye(8)[[3, 1, 7, 0, 2, 6, 4, 5]]
+    Z = rng.integers(-2, 3, (8, 8)).astype(np.float64)
+    S = np.stack([np.ones((8, 8)), np.eye(8), np.zeros((8, 8)), perm, Z, 2.0 * np.ones((8, 8))])
+    out = P.laplace_batch(S)
+    assert list(out[:4]) == [40320.0, 1.0, 0.0, 1.0]
+    assert out[4] == float(O.permanent("glynn", Z.astype(np.int64))[0])
+    assert out[5] == 40320.0 * 256
+    dS = torch.tensor(S, device="cuda")
+    assert np.array_equal(P.laplace_batch(dS).cpu().numpy(), out)
+    flat = torch.empty(S.size + 1, dtype=torch.float64, device="cuda")
+    mis = flat[1:].view(S.shape)
+    mis.copy_(dS)
+    assert np.array_equal(P.laplace_batch(mis).cpu().numpy()[:4], out[:4])
+    Cx = rng.standard_normal((50, 8, 8)) + 1j * rng.standard_normal((50, 8, 8))
+    outc = P.laplace_batch(Cx)
+    for i in (0, 49):
+        ref = O.permanent("glynn", Cx[i])[0]
+        assert scaled_err(outc[i], ref, magsum(Cx[i])) <= TOL
+
+
 def _dd_value(a, alg):
     from paper_2510_03421_b200 import engine as E
 
