@@ -203,23 +203,19 @@ __host__ __device__ constexpr int row_stride() { return (sizeof(T) == 8) ? ((P +
 #endif
 constexpr int kChains = WALK_CHAINS;
 // Per-state-length chain count from a measured sweep on B200
-// (tools/walk_csweep.cu, profiles/r1_chain_sweep.txt): ptxas schedules some
-// lengths markedly better with a different chain count (P = 29, 30, 34: +6%).
-// Only changes worth >= 2% are kept; WALK_CHAINS (default 4) elsewhere.
+// (tools/walk_csweep.cu, profiles/r1_walk_r0_sweep.txt).  With U[0] in
+// registers (walk_r0) 4 chains are within 1% of the best everywhere except
+// P = 25, 43, 44 (6 chains: +5 / +7 / +6%); WALK_CHAINS (default 4) elsewhere.
+template <typename T, int P>
+__host__ __device__ constexpr bool walk_r0();
 template <typename T, int P>
 __host__ __device__ constexpr int walk_chains() {
 #ifdef WALK_CHAINS_FIXED
   return kChains;
 #else
   if constexpr (sizeof(T) == 8) {
-    switch (P) {
-      case 27: case 40: case 44: return 2;
-      case 31: case 37: return 3;
-      case 34: return 5;
-      case 38: return 6;
-      case 29: case 30: return 8;
-      default: return kChains;
-    }
+    if (walk_r0<T, P>()) return (P == 25 || P == 43 || P == 44) ? 6 : kChains;
+    return kChains;
   } else {
     return P == 22 ? 6 : kChains;
   }
@@ -228,6 +224,21 @@ __host__ __device__ constexpr int walk_chains() {
 #ifndef WALK_FUSED
 #define WALK_FUSED 1
 #endif
+// U[0] -- the row flipped at every other step -- held in registers for real
+// walks whose state leaves room (P real state + P row registers under the
+// 255 cap, one 256-thread block per SM).  Measured (tools/walk_p36.cu,
+// tools/walk_csweep.cu -> profiles/r1_walk_r0_sweep.txt): P = 36 Glynn
+// 9.70 -> 8.88 ms per 2^31 steps, 86 -> 94% of the FP64 pipe; P = 17..52
+// gain 5-25% except P = 24 (-5%).  The limiter was short_scoreboard waits
+// on the row loads, not the product chains or occupancy.
+template <typename T, int P>
+__host__ __device__ constexpr bool walk_r0() {
+#ifdef WALK_R0_FORCE
+  return WALK_R0_FORCE && sizeof(T) == 8;
+#else
+  return sizeof(T) == 8 && P >= 17 && P <= 52 && P != 24;
+#endif
+}
 #if WALK_FUSED
 #define WALK_CHUNK walk_chunk_fused
 #else
@@ -266,6 +277,7 @@ __host__ __device__ constexpr int walk_min_blocks() {
 #ifdef WALK_MINB
   return WALK_MINB;
 #endif
+  if (walk_r0<T, P>()) return 1;
   return (Num<T>::kDoubles == 1) ? ((P <= 20) ? 3 : (P <= 41) ? 2 : 1) : ((P <= 14) ? 2 : 1);
 }
 
@@ -332,6 +344,66 @@ __device__ __forceinline__ void term_update(T (&v)[P], const T* __restrict__ row
     acc = (sign > 0) ? Num<T>::add(acc, p) : Num<T>::sub(acc, p);
     if constexpr (MAG) mag += Num<T>::absval(p);
   }
+}
+
+// term_update with the row held in registers (row 0: half of all steps).
+template <typename T, int P, bool W, bool MAG, int UPD>
+__device__ __forceinline__ void term_update_reg(T (&v)[P], const T (&row)[P], int sign, int pc, const double* sW,
+                                                T& acc, double& mag) {
+  constexpr int K = walk_chains<T, P>();
+  constexpr int C = (P < K) ? P : K;
+  T c[C];
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    if (j < C) c[j] = v[j]; else c[j % C] = Num<T>::mul(c[j % C], v[j]);
+    v[j] = (UPD == 0) ? Num<T>::add(v[j], row[j]) : Num<T>::sub(v[j], row[j]);
+  }
+  const T p = tree_of<T, C>(c);
+  if constexpr (W) {
+    const double wt = sW[pc];
+    acc = Num<T>::add(acc, Num<T>::scale(wt, p));
+    if constexpr (MAG) mag += fabs(wt) * Num<T>::absval(p);
+  } else {
+    acc = (sign > 0) ? Num<T>::add(acc, p) : Num<T>::sub(acc, p);
+    if constexpr (MAG) mag += Num<T>::absval(p);
+  }
+}
+
+// walk_chunk_fused with U[0] in registers (u0): the four row-0 steps of
+// every eight read no shared memory.
+template <typename T, int P, bool W, bool MAG>
+__device__ __forceinline__ T walk_chunk_fused_r0(T (&v)[P], const T (&u0)[P], const T* sU, const double* sW,
+                                                 uint64_t k0, uint64_t nq, int pc, double& mag) {
+  constexpr int PS = row_stride<T, P>();
+  T acc = Num<T>::zero();
+  for (uint64_t q = 0; q < nq; ++q) {
+    term_update_reg<T, P, W, MAG, 0>(v, u0, +1, pc, sW, acc, mag);
+    if constexpr (W) ++pc;
+    term_update<T, P, W, MAG, 0>(v, sU + PS, 0.0, -1, pc, sW, acc, mag);
+    if constexpr (W) ++pc;
+    term_update_reg<T, P, W, MAG, 1>(v, u0, +1, pc, sW, acc, mag);
+    if constexpr (W) --pc;
+    const int b3 = (int)(((k0 + (q << 3)) >> 3) & 1);
+    term_update<T, P, W, MAG, 2>(v, sU + 2 * PS, b3 ? -1.0 : 1.0, -1, pc, sW, acc, mag);
+    if constexpr (W) pc += b3 ? -1 : 1;
+    term_update_reg<T, P, W, MAG, 0>(v, u0, +1, pc, sW, acc, mag);
+    if constexpr (W) ++pc;
+    term_update<T, P, W, MAG, 1>(v, sU + PS, 0.0, -1, pc, sW, acc, mag);
+    if constexpr (W) --pc;
+    term_update_reg<T, P, W, MAG, 1>(v, u0, +1, pc, sW, acc, mag);
+    if constexpr (W) --pc;
+    if (q + 1 < nq) {
+      const uint64_t l0 = (q + 1) << 3;
+      const int t = __ffsll((long long)l0) - 1;
+      const uint64_t k = k0 + l0;
+      const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
+      term_update<T, P, W, MAG, 2>(v, sU + t * PS, set ? 1.0 : -1.0, -1, pc, sW, acc, mag);
+      if constexpr (W) pc += set ? 1 : -1;
+    } else {
+      Term<T, P, W, MAG>::add(v, -1, pc, sW, acc, mag);
+    }
+  }
+  return acc;
 }
 
 template <typename T, int P, bool W, bool MAG>
@@ -449,6 +521,11 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_ke
 
   double hi = 0.0, lo = 0.0, hi_i = 0.0, lo_i = 0.0, mag = 0.0;
   const uint64_t total_warps = (uint64_t)gridDim.x * kWalkWarps;
+  T u0[walk_r0<T, P>() ? P : 1];
+  if constexpr (walk_r0<T, P>()) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) u0[j] = sU[j];
+  }
 
   for (uint64_t g = (uint64_t)blockIdx.x * kWalkWarps + warp; g < args.ngroups; g += total_warps) {
     const uint64_t kb = args.k_begin + ((g * 32) << log2L);
@@ -483,8 +560,14 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_ke
       }
     }
     const int pc = __popcll(g0);
-    const T acc = mag_on ? WALK_CHUNK<T, P, W, true>(v, sU, sW, k0, nq, pc, mag)
-                         : WALK_CHUNK<T, P, W, false>(v, sU, sW, k0, nq, pc, mag);
+    T acc;
+    if constexpr (walk_r0<T, P>()) {
+      acc = mag_on ? walk_chunk_fused_r0<T, P, W, true>(v, u0, sU, sW, k0, nq, pc, mag)
+                   : walk_chunk_fused_r0<T, P, W, false>(v, u0, sU, sW, k0, nq, pc, mag);
+    } else {
+      acc = mag_on ? WALK_CHUNK<T, P, W, true>(v, sU, sW, k0, nq, pc, mag)
+                   : WALK_CHUNK<T, P, W, false>(v, sU, sW, k0, nq, pc, mag);
+    }
     dd_acc(hi, lo, Num<T>::re(acc));
     if constexpr (sizeof(T) == 16) dd_acc(hi_i, lo_i, Num<T>::im(acc));
   }

@@ -28,13 +28,16 @@ void one(int B) {
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 4;
   const double ops = (double)(1ull << B) * (sizeof(T) == 8 ? 2 * P : 6 * P - 2);
-  printf("%s %d %d %.3f\n", sizeof(T) == 8 ? "f64" : "c128", P, WALK_CHAINS, ops / (ms * 1e-3) / 1e12);
+  printf("%s %d %d %d %.3f\n", sizeof(T) == 8 ? "f64" : "c128", P, walk_chains<T, P>(), (int)walk_r0<T, P>(),
+         ops / (ms * 1e-3) / 1e12);
   cudaFree(d); cudaFree(parts);
 }
 template <int... Ps> void runf(std::integer_sequence<int, Ps...>) { (one<double, Ps + 12>(std::min(Ps + 11, 29)), ...); }
 template <int... Ps> void runc(std::integer_sequence<int, Ps...>) { (one<cd, Ps + 12>(std::min(Ps + 11, 26)), ...); }
 int main() {
   runf(std::make_integer_sequence<int, 41>{});  // P = 12..52
+#ifndef CSWEEP_F64_ONLY
   runc(std::make_integer_sequence<int, 25>{});  // P = 12..36
+#endif
   return 0;
 }
