@@ -233,6 +233,9 @@ __host__ __device__ constexpr int walk_chains() {
 // on the row loads, not the product chains or occupancy.
 template <typename T, int P>
 __host__ __device__ constexpr bool walk_r0() {
+#ifdef WALK_R0_FORCE_C
+  if (sizeof(T) == 16) return WALK_R0_FORCE_C;
+#endif
 #ifdef WALK_R0_FORCE
   return WALK_R0_FORCE && sizeof(T) == 8;
 #else

@@ -145,3 +145,44 @@ def test_sharded_nccl_single_rank_int():
         np.testing.assert_array_equal(P.sharded_batch(A), P.opt_batch(A))
     finally:
         dist.destroy_process_group()
+
+
+def _range_case(alg, a, span=1 << 22):
+    """GPU raw partial over the last `span` indices of the walk (seeded from
+    high Gray bits) vs the oracle's double-double walk over the same range."""
+    m, n = a.shape
+    total = (1 << (n - 1)) if alg == "glynn" else (1 << n)
+    span = min(span, total // 4)
+    k0, k1 = total - span, total
+    part = S.gpu_partial(alg, a, k0, k1, mag=True)
+    setup = O.walk_setup(alg, a)
+    (rh, rl), (ih, il) = O.walk_dd_mt(setup, k0, k1)
+    gpu = complex(part[0] + part[1], part[2] + part[3])
+    ref = complex(rh + rl, ih + il)
+    return abs(gpu - ref) / max(part[4], 1e-300)
+
+
+@pytest.mark.parametrize("n", list(range(17, 53)) + [56, 62])
+def test_walk_kernels_every_state_length(n):
+    """Every real walk instantiation the C5 n-sweep can reach (P = 17..52 hold
+    U[0] in registers; 56 and 62 do not), on a 2^22-step range at the end of
+    the walk: square Glynn (P = n, B = n-1) and square Ryser (P = B = n)."""
+    rng = np.random.default_rng(1000 + n)
+    a = rng.uniform(-1, 1, (n, n)) / n
+    assert _range_case("glynn", a) <= 1e-11
+    assert _range_case("ryser", a) <= 1e-11
+
+
+@pytest.mark.parametrize("m,n", [(17, 23), (24, 27), (30, 33), (36, 39)])
+def test_weighted_walk_kernels(m, n):
+    """Rectangular Ryser: popcount-weighted walk with P = m state rows."""
+    rng = np.random.default_rng(m * 100 + n)
+    a = rng.uniform(-1, 1, (m, n)) / n
+    assert _range_case("ryser", a) <= 1e-11
+
+
+@pytest.mark.parametrize("n", [20, 24, 28, 32])
+def test_complex_walk_kernels(n):
+    rng = np.random.default_rng(7 * n)
+    a = (rng.uniform(-1, 1, (n, n)) + 1j * rng.uniform(-1, 1, (n, n))) / n
+    assert _range_case("glynn", a) <= 1e-11

@@ -34,7 +34,12 @@ void one(int B) {
 }
 template <int... Ps> void runf(std::integer_sequence<int, Ps...>) { (one<double, Ps + 12>(std::min(Ps + 11, 29)), ...); }
 template <int... Ps> void runc(std::integer_sequence<int, Ps...>) { (one<cd, Ps + 12>(std::min(Ps + 11, 26)), ...); }
+template <int... Ps> void runc2(std::integer_sequence<int, Ps...>) { (one<cd, Ps + 20>(std::min(Ps + 19, 26)), ...); }
 int main() {
+#ifdef CSWEEP_C128_ONLY
+  runc2(std::make_integer_sequence<int, 13>{});  // P = 20..32
+  return 0;
+#endif
   runf(std::make_integer_sequence<int, 41>{});  // P = 12..52
 #ifndef CSWEEP_F64_ONLY
   runc(std::make_integer_sequence<int, 25>{});  // P = 12..36
