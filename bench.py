@@ -251,6 +251,30 @@ def run_engine(args):
         dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     e2e_value = steps_total * args.steps / float(e2e.item())
 
+    # ---- n-sweep (the metric's "n = 20-36"): single-GPU walks on rank 0,
+    # same seeded law (SURVEY 8(d) k = 10 + n), device time per permanent
+    sweep = {}
+    if rank == 0:
+        for ns in (20, 24, 28, 32):
+            asw = W.c5(ns)
+            tot = 1 << (ns - 1)
+            for _ in range(3):
+                gpu_partial("glynn", asw, 0, tot, False, device_out=part, stream=stream.cuda_stream)
+            reps = 5
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            kms = []
+            for _ in range(reps):
+                gpu_partial("glynn", asw, 0, tot, False, device_out=part, stream=stream.cuda_stream)
+                kms.append(lib.perm_last_kernel_ms())
+            e1.record(stream)
+            torch.cuda.synchronize()
+            call_ms = e0.elapsed_time(e1) / reps
+            kern = statistics.mean(kms)
+            sweep[str(ns)] = {"kernel_ms": kern, "call_ms": call_ms, "steps_per_s_kernel": tot / (kern * 1e-3),
+                              "frac_of_pipe": tot * 2 * ns / (kern * 1e-3) / peak_pipe}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
@@ -281,7 +305,8 @@ def run_engine(args):
                        "parallelism": f"gray-range shards x{world} (NCCL all-gather of 8-double partials)",
                        "l2": "flushed (256 MiB write) before every step, outside the timed events",
                        "launch": {"grid": grid.value, "threads": 256, "log2_chunk": log2L.value},
-                       "value_check": value_check},
+                       "value_check": value_check,
+                       "n_sweep_1gpu": sweep},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_pipe, "unit": "FP64 op/s",
                          "frac": achieved / peak_pipe, "frac_of_fma_peak": achieved / peak_dfma,
                          "frac_of_nominal": achieved / NOMINAL_DFMA,
