@@ -110,11 +110,7 @@ int main() {
     printf("classic glynn 8x8: %.4f ms  %.0f GB/s\n", ms, B * 520.0 / (ms * 1e-3) / 1e9);
     run_bulk<8, 8, 64, 3, Laplace8OpT<4, 1, 1>>("lap8 w4", a, out, B, nsm, 4, ref, scale);
     run_bulk<8, 8, 64, 3, Laplace8OpT<4, 1, 1>, true>("CO w4", a, out, B, nsm, 4, ref, scale);
-    run_bulk<8, 8, 64, 3, Laplace8OpT<3, 1, 1>>("lap8 w3", a, out, B, nsm, 4, ref, scale);
-    run_bulk<8, 8, 64, 3, Laplace8OpT<6, 1, 1>>("lap8 w6", a, out, B, nsm, 4, ref, scale);
-    run_bulk<8, 8, 64, 3, Laplace8OpT<2, 1, 1>>("lap8 w2", a, out, B, nsm, 4, ref, scale);
-    run_bulk<8, 8, 128, 2, Laplace8OpT<4, 1, 1>>("lap8 w4", a, out, B, nsm, 2, ref, scale);
-    run_warp<8, 8, 8, 3, Laplace8OpT<4, 1, 1>>("lap8 w4", a, out, B, nsm, 1, ref, scale);
+    run_bulk<8, 8, 64, 3, Laplace8OpT<5, 1, 0>>("lap8 full", a, out, B, nsm, 4, ref, scale);
     {
       const int64_t b2 = 150000;
       float ms2 = timeit([&] { batch_glynn_kernel<double, 8><<<(b2 + kBatchThreads - 1) / kBatchThreads, kBatchThreads, smem>>>(a, out, b2); }, 10);
