@@ -374,6 +374,35 @@ __device__ __forceinline__ int64_t exact_d2ll(double x) {
   return __double_as_longlong(x + 6755399441055744.0) - 0x4338000000000000LL;
 }
 
+// signed 64 x 64 -> 128 (exact)
+__device__ __forceinline__ i128 i128_mul_s64s64(int64_t a, int64_t b) {
+  i128 r;
+  r.lo = (uint64_t)a * (uint64_t)b;
+  r.hi = (uint64_t)__mul64hi(a, b);
+  return r;
+}
+
+// The group products as int64, multiplied as a pairwise tree: exact signed
+// 64x64->128 products of neighbouring groups, then mod-2^128 products of
+// those (P = 32: 2 wide products + 1 mod-2^128 product instead of 3
+// i128 x int64 products in a chain).
+template <int NG>
+__device__ __forceinline__ i128 group_product_i128(const int64_t (&c)[NG]) {
+  if constexpr (NG == 1) {
+    return i128_from(c[0]);
+  } else if constexpr (NG == 2) {
+    return i128_mul_s64s64(c[0], c[1]);
+  } else if constexpr (NG == 3) {
+    return i128_mul_s64(i128_mul_s64s64(c[0], c[1]), c[2]);
+  } else {
+    i128 p = i128_mul(i128_mul_s64s64(c[0], c[1]), i128_mul_s64s64(c[2], c[3]));
+#pragma unroll
+    for (int q = 4; q + 1 < NG; q += 2) p = i128_mul(p, i128_mul_s64s64(c[q], c[q + 1]));
+    if constexpr (NG > 4 && (NG & 1)) p = i128_mul_s64(p, c[NG - 1]);
+    return p;
+  }
+}
+
 template <int P>
 __device__ __forceinline__ void fp_term(const double (&v)[P], bool neg, i128& acc, double& est, double& mag) {
   constexpr int NG = (P + 7) / 8;
@@ -385,13 +414,13 @@ __device__ __forceinline__ void fp_term(const double (&v)[P], bool neg, i128& ac
     for (int j = 8 * q + 1; j < 8 * q + 8 && j < P; ++j) x *= v[j];
     g[q] = x;
   }
-  i128 p = i128_from(exact_d2ll(g[0]));
+  int64_t c[NG];
   double f = g[0];
 #pragma unroll
-  for (int q = 1; q < NG; ++q) {
-    p = i128_mul_s64(p, exact_d2ll(g[q]));
-    f *= g[q];
-  }
+  for (int q = 0; q < NG; ++q) c[q] = exact_d2ll(g[q]);
+#pragma unroll
+  for (int q = 1; q < NG; ++q) f *= g[q];
+  const i128 p = group_product_i128<NG>(c);
   if (neg) {
     acc = i128_sub(acc, p);
     est -= f;
@@ -416,6 +445,9 @@ __global__ void __launch_bounds__(kIntThreads, INT_FP_MINB) int_walk_wrap_fp_ker
   const uint64_t nq = (1ull << a.log2L) >> 3;
   i128 acc = i128_from(0);
   double hi = 0.0, lo = 0.0, mag = 0.0;
+  // (U[0] in registers, as in the float walk, measured slower here: C4a
+  // 15.5 -> 16.8 ms at 255 registers)
+#define INT_ROW0(op) row_##op<double, P>(v, sU);
   const uint64_t nthr = (uint64_t)gridDim.x * kIntThreads;
   for (uint64_t c = (uint64_t)blockIdx.x * kIntThreads + threadIdx.x; c < a.nchunks; c += nthr) {
     const uint64_t k0 = a.k_begin + (c << a.log2L);
@@ -435,22 +467,23 @@ __global__ void __launch_bounds__(kIntThreads, INT_FP_MINB) int_walk_wrap_fp_ker
         row_fma<double, P>(v, set ? 1.0 : -1.0, sU + t * PS);
       }
       fp_term<P>(v, false, acc, est, mag);
-      row_add<double, P>(v, sU);
+      INT_ROW0(add);
       fp_term<P>(v, true, acc, est, mag);
       row_add<double, P>(v, sU + PS);
       fp_term<P>(v, false, acc, est, mag);
-      row_sub<double, P>(v, sU);
+      INT_ROW0(sub);
       fp_term<P>(v, true, acc, est, mag);
       row_fma<double, P>(v, (((k0 + l0) >> 3) & 1) ? -1.0 : 1.0, sU + 2 * PS);
       fp_term<P>(v, false, acc, est, mag);
-      row_add<double, P>(v, sU);
+      INT_ROW0(add);
       fp_term<P>(v, true, acc, est, mag);
       row_sub<double, P>(v, sU + PS);
       fp_term<P>(v, false, acc, est, mag);
-      row_sub<double, P>(v, sU);
+      INT_ROW0(sub);
       fp_term<P>(v, true, acc, est, mag);
     }
     dd_acc(hi, lo, est);
+#undef INT_ROW0
   }
   for (int off = 16; off > 0; off >>= 1) {
     acc = i128_add(acc, shfl_down_i128(acc, off));
