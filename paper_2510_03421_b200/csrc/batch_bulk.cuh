@@ -323,54 +323,9 @@ __host__ __device__ constexpr LpSub lp_sub(int p) {
       }
   return s;
 }
-// per(H[:, {a,b,c,d}]) of a 4-row half H from its row-pair tables qa (rows 0,1),
-// qb (rows 2,3): the 6 ordered splits of {a,b,c,d} into two pairs.  CH = 2
-// runs them as two 3-deep chains (one extra add, half the dependency depth).
-template <int CH, int a, int b, int c, int d>
-__device__ __forceinline__ double lp_minor(const double (&qa)[28], const double (&qb)[28]) {
-  if constexpr (CH == 1) {
-    double g = qa[lp_pidx(a, b)] * qb[lp_pidx(c, d)];
-    g = fma(qa[lp_pidx(c, d)], qb[lp_pidx(a, b)], g);
-    g = fma(qa[lp_pidx(a, c)], qb[lp_pidx(b, d)], g);
-    g = fma(qa[lp_pidx(b, d)], qb[lp_pidx(a, c)], g);
-    g = fma(qa[lp_pidx(a, d)], qb[lp_pidx(b, c)], g);
-    g = fma(qa[lp_pidx(b, c)], qb[lp_pidx(a, d)], g);
-    return g;
-  } else {
-    double g = qa[lp_pidx(a, b)] * qb[lp_pidx(c, d)];
-    double h = qa[lp_pidx(b, d)] * qb[lp_pidx(a, c)];
-    g = fma(qa[lp_pidx(c, d)], qb[lp_pidx(a, b)], g);
-    h = fma(qa[lp_pidx(a, d)], qb[lp_pidx(b, c)], h);
-    g = fma(qa[lp_pidx(a, c)], qb[lp_pidx(b, d)], g);
-    h = fma(qa[lp_pidx(b, c)], qb[lp_pidx(a, d)], h);
-    return g + h;
-  }
-}
-// pairs P0 .. P0+G-1 of (X, X^c): all 2G minors first, then the 2G shuffles
-// with the partner lane (the other half of the same matrix), then the 2G
-// products -- G pairs of independent work between dependent steps
-template <int CH, int P0, int... Is>
-__device__ __forceinline__ void lp_group(const double (&qa)[28], const double (&qb)[28], double (&acc)[4],
-                                         std::integer_sequence<int, Is...>) {
-  constexpr int G = sizeof...(Is);
-  double g[2 * G], h[2 * G];
-  ((g[2 * Is] = lp_minor<CH, lp_sub(P0 + Is).x[0], lp_sub(P0 + Is).x[1], lp_sub(P0 + Is).x[2], lp_sub(P0 + Is).x[3]>(qa, qb),
-    g[2 * Is + 1] =
-        lp_minor<CH, lp_sub(P0 + Is).c[0], lp_sub(P0 + Is).c[1], lp_sub(P0 + Is).c[2], lp_sub(P0 + Is).c[3]>(qa, qb)),
-   ...);
-#pragma unroll
-  for (int i = 0; i < 2 * G; ++i) h[i] = __shfl_xor_sync(0xffffffffu, g[i], 1);
-#pragma unroll
-  for (int i = 0; i < G; ++i) {
-    acc[i & 3] = fma(g[2 * i], h[2 * i + 1], acc[i & 3]);
-    acc[i & 3] = fma(g[2 * i + 1], h[2 * i], acc[i & 3]);
-  }
-}
-template <int CH, int G, int... Ks>
-__device__ __forceinline__ void lp_all(const double (&qa)[28], const double (&qb)[28], double (&acc)[4],
-                                       std::integer_sequence<int, Ks...>) {
-  (lp_group<CH, Ks * G>(qa, qb, acc, std::make_integer_sequence<int, (35 - Ks * G < G) ? 35 - Ks * G : G>{}), ...);
-}
+// per(H[:, {a,b,c,d}]) of a 4-row half H from its row-pair tables qa (rows
+// 0,1) and qb (rows 2,3) is the sum over the 6 ordered splits of {a,b,c,d}
+// into two pairs, qa(pair) * qb(other pair): one DMUL + five DFMAs.
 // Half exchange: the top lane accumulates pairs 0..17, the bottom lane pairs
 // 18..34; at step i each lane sends the partner the two minors the partner
 // needs (selected by lane half), so every 32-bit shuffle carries useful data
@@ -447,7 +402,7 @@ __device__ __forceinline__ void lp_qtable(const double (&v)[16], double (&q)[28]
     for (int k = i + 1; k < 8; ++k) q[lp_pidx(i, k)] = fma(v[i], v[8 + k], v[k] * v[8 + i]);
 }
 
-template <int G, int CH, int XCH = 1>
+template <int G>
 struct Laplace8OpT {
   static constexpr int kLanes = 2;
   template <class R>
@@ -484,20 +439,14 @@ struct Laplace8OpT {
       lp_qtable(v, qb);
     }
     release();  // the tables are all this lane needs: free the slot before the minors
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    if constexpr (XCH == 0) {
-      lp_all<CH, G>(qa, qb, acc, std::make_integer_sequence<int, (35 + G - 1) / G>{});
-      if (half == 0 && mat < cnt) out[first + mat] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-    } else {
-      double acc8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      lp_wide_all<G>(qa, qb, half != 0, acc8, std::make_integer_sequence<int, (18 + G - 1) / G>{});
-      const double mine = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
-      const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
-      if (half == 0 && mat < cnt) out[first + mat] = mine + other;
-    }
+    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    lp_wide_all<G>(qa, qb, half != 0, acc, std::make_integer_sequence<int, (18 + G - 1) / G>{});
+    const double mine = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
+    if (half == 0 && mat < cnt) out[first + mat] = mine + other;
   }
 };
 
-using Laplace8Op = Laplace8OpT<4, 1, 1>;
+using Laplace8Op = Laplace8OpT<4>;  // 4 steps = 16 minors per group
 
 }  // namespace permb200

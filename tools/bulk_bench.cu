@@ -108,9 +108,10 @@ int main() {
       scale[i] = p * 40320.0 / 16777216.0;  // ~ per(|A|)
     }
     printf("classic glynn 8x8: %.4f ms  %.0f GB/s\n", ms, B * 520.0 / (ms * 1e-3) / 1e9);
-    run_bulk<8, 8, 64, 3, Laplace8OpT<4, 1, 1>>("lap8 w4", a, out, B, nsm, 4, ref, scale);
-    run_bulk<8, 8, 64, 3, Laplace8OpT<4, 1, 1>, true>("CO w4", a, out, B, nsm, 4, ref, scale);
-    run_bulk<8, 8, 64, 3, Laplace8OpT<5, 1, 0>>("lap8 full", a, out, B, nsm, 4, ref, scale);
+    run_bulk<8, 8, 64, 3, Laplace8OpT<4>>("lap8 w4", a, out, B, nsm, 4, ref, scale);
+    run_bulk<8, 8, 64, 3, Laplace8OpT<4>, true>("CO w4", a, out, B, nsm, 4, ref, scale);
+    run_bulk<8, 8, 64, 3, Laplace8OpT<2>>("lap8 w2", a, out, B, nsm, 4, ref, scale);
+    run_bulk<8, 8, 64, 3, Laplace8OpT<6>>("lap8 w6", a, out, B, nsm, 4, ref, scale);
     {
       const int64_t b2 = 150000;
       float ms2 = timeit([&] { batch_glynn_kernel<double, 8><<<(b2 + kBatchThreads - 1) / kBatchThreads, kBatchThreads, smem>>>(a, out, b2); }, 10);
