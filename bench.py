@@ -255,25 +255,27 @@ def run_engine(args):
     # same seeded law (SURVEY 8(d) k = 10 + n), device time per permanent
     sweep = {}
     if rank == 0:
-        for ns in (20, 24, 28, 32):
+        for alg, ns in (("glynn", 20), ("glynn", 24), ("glynn", 28), ("glynn", 32), ("ryser", 28), ("ryser", 32)):
             asw = W.c5(ns)
-            tot = 1 << (ns - 1)
+            tot = (1 << (ns - 1)) if alg == "glynn" else (1 << ns)
             for _ in range(3):
-                gpu_partial("glynn", asw, 0, tot, False, device_out=part, stream=stream.cuda_stream)
+                gpu_partial(alg, asw, 0, tot, False, device_out=part, stream=stream.cuda_stream)
             reps = 5
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record(stream)
             kms = []
             for _ in range(reps):
-                gpu_partial("glynn", asw, 0, tot, False, device_out=part, stream=stream.cuda_stream)
+                gpu_partial(alg, asw, 0, tot, False, device_out=part, stream=stream.cuda_stream)
                 kms.append(lib.perm_last_kernel_ms())
             e1.record(stream)
             torch.cuda.synchronize()
             call_ms = e0.elapsed_time(e1) / reps
             kern = statistics.mean(kms)
-            sweep[str(ns)] = {"kernel_ms": kern, "call_ms": call_ms, "steps_per_s_kernel": tot / (kern * 1e-3),
-                              "frac_of_pipe": tot * 2 * ns / (kern * 1e-3) / peak_pipe}
+            key = str(ns) if alg == "glynn" else f"ryser_{ns}"
+            sweep[key] = {"kernel_ms": kern, "call_ms": call_ms,
+                          ("steps_per_s_kernel" if alg == "glynn" else "subsets_per_s_kernel"): tot / (kern * 1e-3),
+                          "frac_of_pipe": tot * 2 * ns / (kern * 1e-3) / peak_pipe}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
