@@ -406,13 +406,21 @@ __device__ __forceinline__ i128 group_product_i128(const int64_t (&c)[NG]) {
 template <int P>
 __device__ __forceinline__ void fp_term(const double (&v)[P], bool neg, i128& acc, double& est, double& mag) {
   constexpr int NG = (P + 7) / 8;
+  // group products as balanced trees (depth 3, not a 7-deep DMUL chain):
+  // every sub-product of a group is itself an exact integer < 2^51, so the
+  // order is free, and B200's FP64 pipe wants many independent DMULs in a row
   double g[NG];
 #pragma unroll
   for (int q = 0; q < NG; ++q) {
-    double x = v[8 * q];
+    constexpr int W = 8;
+    double t[W];
 #pragma unroll
-    for (int j = 8 * q + 1; j < 8 * q + 8 && j < P; ++j) x *= v[j];
-    g[q] = x;
+    for (int j = 0; j < W; ++j) t[j] = (8 * q + j < P) ? v[8 * q + j] : 1.0;
+#pragma unroll
+    for (int h = 1; h < W; h <<= 1)
+#pragma unroll
+      for (int j = 0; j + h < W; j += 2 * h) t[j] *= t[j + h];
+    g[q] = t[0];
   }
   int64_t c[NG];
   double f = g[0];
