@@ -1,6 +1,8 @@
 // Host-side planning and launch of the Gray-walk kernels.
 #pragma once
+#include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <utility>
 
 #include "walk.cuh"
@@ -32,6 +34,11 @@ struct WalkPlan {
 
 using walk_fn = cudaError_t (*)(const WalkJob&, WalkPlan*, cudaStream_t);
 
+#ifndef WALK_DEFAULT_MAX_LOG2L
+#define WALK_DEFAULT_MAX_LOG2L 10  // accuracy: C5 relative error 8.5e-10 at 2^11, 4.1e-10 at 2^10 (+0.4% time)
+#endif
+constexpr int kWalkDefaultMaxLog2L = WALK_DEFAULT_MAX_LOG2L;
+
 // Upper bound on block partials any plan writes (grid <= 148 * 8).
 constexpr int kMaxPartials = 148 * 16;
 
@@ -57,6 +64,18 @@ inline int choose_log2L(uint64_t steps, uint64_t lanes, int per_group = 32) {
     }
   }
   return best;
+}
+
+// Upper bound on the chunk length exponent: the state drifts by rounding over
+// the L updates of a chunk (it is re-seeded exactly at each chunk start), so
+// L also sets the walk's accuracy.  PERM_WALK_MAX_LOG2L overrides (tuning).
+inline int walk_max_log2L() {
+  static const int v = [] {
+    const char* e = std::getenv("PERM_WALK_MAX_LOG2L");
+    const int x = (e && *e) ? std::atoi(e) : kWalkDefaultMaxLog2L;
+    return x < 3 ? 3 : (x > 14 ? 14 : x);
+  }();
+  return v;
 }
 
 // Largest power-of-two alignment that divides x (x != 0), capped.
@@ -98,7 +117,7 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
   if (bps * nsm > kMaxPartials) bps = kMaxPartials / nsm;
   const uint64_t lanes = (uint64_t)bps * nsm * kWalkThreads;
   // alignment: chunks of L must tile [k_begin, k_end) in groups of 32
-  int r = job.force_log2L > 0 ? job.force_log2L : choose_log2L(steps, lanes);
+  int r = job.force_log2L > 0 ? job.force_log2L : std::min(choose_log2L(steps, lanes), walk_max_log2L());
   const int amax = std::min(align_log2(job.k_begin), align_log2(steps)) - 5;
   if (r > amax) r = amax;
   if (r < 3 || (steps >> r) < 32) {
