@@ -43,7 +43,7 @@ enum {
 /* algorithm ids, same order as AlgorithmId in src/algorithms.py:26-31 */
 enum { PERM_ALG_COMBINATORIC = 0, PERM_ALG_RYSER = 1, PERM_ALG_GLYNN = 2 };
 /* batch-only formulas (perm_batch_*; no reference counterpart, exact algebra):
- * PARTITION = Moebius inversion over set partitions of the rows, m <= 4;
+ * PARTITION = Moebius inversion over set partitions of the rows, m <= 6 (complex m <= 4);
  * LAPLACE = 4+4-row Laplace expansion from 2x2 row-pair permanents, 8x8 real. */
 enum { PERM_ALG_BATCH_PARTITION = 3, PERM_ALG_BATCH_LAPLACE = 4 };
 
@@ -127,8 +127,8 @@ int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int
  * a = [B][m][n] row-major contiguous (host, or device if dev_ptr = 1),
  * out = [B] (same memory space).  alg = PERM_ALG_* (incl. the batch-only
  * formulas) or -1 for the batch dispatch (perm_batch_select: LAPLACE for 8x8
- * real, Glynn for other squares, PARTITION for m <= 4 < n, subset-skipping
- * Ryser otherwise).  PARTITION / LAPLACE stream the batch through shared
+ * real, Glynn for other squares, PARTITION for m <= 4 < n and for m = 5, 6
+ * with n >= m + 2, subset-skipping Ryser otherwise).  PARTITION / LAPLACE stream the batch through shared
  * memory with 1-D bulk copies (persistent grid); other algorithms run one
  * thread (or warp) per matrix.
  * Requires m <= n <= 16.  Device-pointer calls are asynchronous on `stream`. */

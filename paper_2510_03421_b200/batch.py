@@ -7,7 +7,7 @@ The reference has no batch entry point -- ``as_matrix`` rejects anything but
 permanents with one kernel launch (C ABI perm_batch_*).  The batch dispatch
 (``opt_batch``) uses two batch-only exact formulas that are cheaper per
 matrix than any of the reference's algorithms: the set-partition (Moebius)
-formula for m <= 4 and the 4+4 Laplace expansion for 8x8, both streamed
+formula for m <= 6 and the 4+4 Laplace expansion for 8x8, both streamed
 through shared memory by bulk copies (csrc/batch_bulk.cuh).
 
 Float64 / complex128 batches only; integer batches are routed through the
@@ -81,12 +81,13 @@ def _run(a, alg):
 def opt_batch(a, params=None):
     """Permanents of a [B, m, n] batch with the batch dispatch
     (perm_batch_select: Laplace for 8x8 real, Glynn for other squares, the
-    partition formula for m <= 4, subset-skipping Ryser otherwise)."""
+    partition formula for m <= 4 < n and m = 5, 6 with n >= m + 2,
+    subset-skipping Ryser otherwise)."""
     return _run(a, None)
 
 
 def partition_batch(a):
-    """m <= 4: sum over set partitions pi of the rows of
+    """m <= 6 (complex m <= 4): sum over set partitions pi of the rows of
     mu(pi) prod_{blocks b} sum_j prod_{i in b} a_ij."""
     return _run(a, "partition")
 

@@ -200,7 +200,74 @@ __host__ __device__ constexpr int bb_hibit(int x) {
   return h;
 }
 
-// per of an M x N matrix (M <= 4) from the subset sums S[b] = sum_j prod_{i in b} a_ij
+// Set partitions of {0..M-1} (M <= 6, Bell(6) = 203) with their Moebius
+// coefficients, generated at compile time from restricted growth strings.
+struct BbParts {
+  int n;
+  int nb[256];
+  int blk[256][6];
+  int coef[256];
+};
+template <int M>
+__host__ __device__ constexpr BbParts bb_parts() {
+  BbParts P{};
+  int a[6] = {0, 0, 0, 0, 0, 0};
+  for (;;) {
+    int nb = 0;
+    for (int i = 0; i < M; ++i) nb = (a[i] + 1 > nb) ? a[i] + 1 : nb;
+    int masks[6] = {0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < M; ++i) masks[a[i]] |= 1 << i;
+    int c = 1;
+    for (int b = 0; b < nb; ++b) {
+      int sz = 0;
+      for (int i = 0; i < M; ++i) sz += (masks[b] >> i) & 1;
+      for (int f = 2; f < sz; ++f) c *= f;  // (|b| - 1)!
+      if ((sz - 1) & 1) c = -c;
+    }
+    P.nb[P.n] = nb;
+    for (int b = 0; b < 6; ++b) P.blk[P.n][b] = (b < nb) ? masks[b] : 0;
+    P.coef[P.n] = c;
+    ++P.n;
+    int i = M - 1;  // next restricted growth string
+    for (; i > 0; --i) {
+      int mx = 0;
+      for (int j = 0; j < i; ++j) mx = (a[j] > mx) ? a[j] : mx;
+      if (a[i] <= mx) {
+        ++a[i];
+        for (int j = i + 1; j < M; ++j) a[j] = 0;
+        break;
+      }
+    }
+    if (i == 0) break;
+  }
+  return P;
+}
+template <int M>
+struct BbPartsOf {
+  static constexpr BbParts value = bb_parts<M>();
+};
+template <typename T, int M, int Q>
+__device__ __forceinline__ T bb_part_term(const T (&S)[1 << M]) {
+  using X = Num<T>;
+  constexpr int nb = BbPartsOf<M>::value.nb[Q];
+  constexpr int c = BbPartsOf<M>::value.coef[Q];
+  T prod = S[BbPartsOf<M>::value.blk[Q][0]];
+  if constexpr (nb > 1) prod = X::mul(prod, S[BbPartsOf<M>::value.blk[Q][1]]);
+  if constexpr (nb > 2) prod = X::mul(prod, S[BbPartsOf<M>::value.blk[Q][2]]);
+  if constexpr (nb > 3) prod = X::mul(prod, S[BbPartsOf<M>::value.blk[Q][3]]);
+  if constexpr (nb > 4) prod = X::mul(prod, S[BbPartsOf<M>::value.blk[Q][4]]);
+  if constexpr (nb > 5) prod = X::mul(prod, S[BbPartsOf<M>::value.blk[Q][5]]);
+  return (c == 1) ? prod : X::scale((double)c, prod);
+}
+template <typename T, int M, int... Qs>
+__device__ __forceinline__ T bb_combine_generic(const T (&S)[1 << M], std::integer_sequence<int, Qs...>) {
+  T acc[4] = {Num<T>::zero(), Num<T>::zero(), Num<T>::zero(), Num<T>::zero()};
+  ((acc[Qs & 3] = Num<T>::add(acc[Qs & 3], bb_part_term<T, M, Qs>(S))), ...);
+  return Num<T>::add(Num<T>::add(acc[0], acc[1]), Num<T>::add(acc[2], acc[3]));
+}
+
+// per of an M x N matrix from the subset sums S[b] = sum_j prod_{i in b} a_ij
+// (M <= 4 written out with shared sub-products; M = 5, 6 from the table)
 template <typename T, int M>
 __device__ __forceinline__ T partition_combine(const T (&S)[1 << M]) {
   using X = Num<T>;
@@ -215,8 +282,9 @@ __device__ __forceinline__ T partition_combine(const T (&S)[1 << M]) {
     r = X::sub(r, X::mul(S[5], S[2]));
     r = X::sub(r, X::mul(S[6], S[1]));
     return X::add(r, X::scale(2.0, S[7]));
+  } else if constexpr (M >= 5) {
+    return bb_combine_generic<T, M>(S, std::make_integer_sequence<int, BbPartsOf<M>::value.n>{});
   } else {
-    static_assert(M == 4, "partition formula kernel covers m <= 4");
     // singletons: p0p1p2p3
     const T s01 = X::mul(S[1], S[2]), s23 = X::mul(S[4], S[8]);
     T r = X::mul(s01, s23);
@@ -246,7 +314,7 @@ __device__ __forceinline__ T partition_combine(const T (&S)[1 << M]) {
 template <typename T, int M, int N>
 struct PartitionOp {
   static constexpr int kLanes = 1;
-  static_assert(M >= 1 && M <= 4 && M <= N, "m <= 4, m <= n");
+  static_assert(M >= 1 && M <= 6 && M <= N, "m <= 6, m <= n");
   static_assert((N * sizeof(T)) % 16 == 0 || sizeof(T) == 16, "rows read as 16-byte chunks");
   template <class R>
   __device__ __forceinline__ static void run(const T* tile, int64_t first, int cnt, T* out, int me, R&& release) {

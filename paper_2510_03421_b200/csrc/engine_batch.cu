@@ -137,7 +137,9 @@ static int launch_batch(int alg, bool cplx, int64_t B, int m, int n, const void*
   if (alg == PERM_ALG_BATCH_LAPLACE || alg == PERM_ALG_BATCH_PARTITION) {
     const int st = launch_bulk_batch(alg, cplx, B, m, n, dA, dOut, stream);
     if (st >= 0) return st;
-    alg = (alg == PERM_ALG_BATCH_LAPLACE) ? PERM_ALG_GLYNN : PERM_ALG_COMBINATORIC;
+    alg = (alg == PERM_ALG_BATCH_LAPLACE) ? PERM_ALG_GLYNN
+          : (m <= 4)                      ? PERM_ALG_COMBINATORIC  // memoized DP
+                                          : PERM_ALG_RYSER;        // subset-skipping
   }
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -275,11 +277,13 @@ static void par_memcpy(void* dst, const void* src, size_t bytes) {
 int batch_select(int m, int n) {
   // cheapest exact per-matrix work: the 4+4 Laplace kernel for 8x8 (1134
   // flops against Glynn's 2048; complex 8x8 falls back to Glynn), Glynn for
-  // other squares, the partition formula for m <= 4 (C2b: 290 flops), the
-  // subset-skipping Ryser else
+  // other squares, the partition formula for m <= 4 (C2b: 290 flops) and for
+  // m = 5, 6 with n >= m + 2 (5x10: ~830 flops against ~8300 for the
+  // subset-skipping Ryser), that Ryser else
   if (m == 8 && n == 8) return PERM_ALG_BATCH_LAPLACE;
   if (m == n) return PERM_ALG_GLYNN;
-  return (m <= 4) ? (int)PERM_ALG_BATCH_PARTITION : (int)PERM_ALG_RYSER;
+  if (m <= 4 || (m <= 6 && n >= m + 2)) return PERM_ALG_BATCH_PARTITION;
+  return PERM_ALG_RYSER;
 }
 
 int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a, double* out, int dev_ptr,
@@ -302,8 +306,8 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
     set_error("the Laplace batch formula is 8x8 only");
     return PERM_BAD_SHAPE;
   }
-  if (alg == PERM_ALG_BATCH_PARTITION && m > 4) {
-    set_error("the partition batch formula needs m <= 4");
+  if (alg == PERM_ALG_BATCH_PARTITION && m > 6) {
+    set_error("the partition batch formula needs m <= 6");
     return PERM_BAD_SHAPE;
   }
   if (alg == PERM_ALG_BATCH_LAPLACE && cplx) alg = PERM_ALG_GLYNN;

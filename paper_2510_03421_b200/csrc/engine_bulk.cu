@@ -1,5 +1,5 @@
 // Host side of the bulk-pipelined batch kernels (batch_bulk.cuh): the
-// partition-formula kernel for m <= 4 and the 4+4 Laplace kernel for 8x8,
+// partition-formula kernel for m <= 6 and the 4+4 Laplace kernel for 8x8,
 // picked by the batch dispatch (perm_batch_select) for device-resident
 // batches that meet the 1-D bulk-copy rules (16-byte aligned base, matrix
 // size a multiple of 16 bytes).
@@ -32,13 +32,16 @@ int sm_count() {
   return n;
 }
 
-// Tile shape from the matrix size: <= ~40 KB per stage, two stages, two
-// blocks per SM (measured on C2b: 4x10 f64, 128 threads, 6.0 TB/s).
+// Tile shape from the matrix size: <= ~40 KB per stage, two stages; as many
+// blocks per SM as ~200 KB of shared memory holds, at most 8 (C2b: 4x10
+// f64, 128 threads, 2 blocks per SM, 6.0 TB/s).
 template <typename T, int M, int N>
 struct PartCfg {
   static constexpr int kBytes = M * N * (int)sizeof(T);
   static constexpr int kTPB = kBytes <= 320 ? 128 : (kBytes <= 640 ? 64 : 32);
   static constexpr int kStages = 2;
+  static constexpr int kSmem = kStages * kTPB * kBytes;
+  static constexpr int kPerSM = (200 * 1024 / kSmem < 1) ? 1 : (200 * 1024 / kSmem > 8 ? 8 : 200 * 1024 / kSmem);
 };
 
 template <typename T, int M, int N>
@@ -53,7 +56,7 @@ cudaError_t launch_partition(const void* a, void* out, int64_t B, cudaStream_t s
     attr[cur_device()] = true;
   }
   const int64_t ntiles = (B + Cfg::kTPB - 1) / Cfg::kTPB;
-  const int grid = (int)std::min<int64_t>(ntiles, 2 * (int64_t)sm_count());
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)Cfg::kPerSM * sm_count());
   k<<<grid, Cfg::kTPB, smem, s>>>(static_cast<const T*>(a), static_cast<T*>(out), B);
   return cudaGetLastError();
 }
@@ -78,11 +81,13 @@ cudaError_t launch_laplace8(const void* a, void* out, int64_t B, cudaStream_t s)
   return cudaGetLastError();
 }
 
-// (M, N), 1 <= M <= 4, M <= N <= 16: IDX = (M-1)*16 + (N-1); f64 needs even N
+// (M, N), 1 <= M <= 6, M <= N <= 16: IDX = (M-1)*16 + (N-1); f64 needs even
+// N (16-byte row chunks); complex stops at M = 4 (the 2^M complex subset sums
+// would not fit in registers)
 template <typename T, int I>
 bulk_fn part_entry() {
   constexpr int M = I / 16 + 1, N = I % 16 + 1;
-  if constexpr (N >= M && (sizeof(T) == 16 || N % 2 == 0)) return &launch_partition<T, M, N>;
+  if constexpr (N >= M && (sizeof(T) == 16 ? M <= 4 : N % 2 == 0)) return &launch_partition<T, M, N>;
   else return nullptr;
 }
 template <typename T, int... Is>
@@ -96,7 +101,8 @@ bulk_fn pick_partition(int m, int n, std::integer_sequence<int, Is...>) {
 
 bool bulk_batch_supported(int alg, bool cplx, int m, int n) {
   if (alg == PERM_ALG_BATCH_LAPLACE) return !cplx && m == 8 && n == 8;
-  if (alg == PERM_ALG_BATCH_PARTITION) return m >= 1 && m <= 4 && m <= n && n <= 16 && (cplx || n % 2 == 0);
+  if (alg == PERM_ALG_BATCH_PARTITION)
+    return m >= 1 && m <= n && n <= 16 && (cplx ? m <= 4 : (m <= 6 && n % 2 == 0));
   return false;
 }
 
@@ -110,7 +116,7 @@ int launch_bulk_batch(int alg, bool cplx, int64_t B, int m, int n, const void* d
     fn = &launch_laplace8;
   } else {
     fn = cplx ? pick_partition<cd>(m, n, std::make_integer_sequence<int, 64>{})
-              : pick_partition<double>(m, n, std::make_integer_sequence<int, 64>{});
+              : pick_partition<double>(m, n, std::make_integer_sequence<int, 96>{});
   }
   if (!fn) return -1;
   const cudaError_t e = fn(dA, dOut, B, stream);

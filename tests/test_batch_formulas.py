@@ -1,7 +1,7 @@
 """The two batch-only formulas of csrc/batch_bulk.cuh, restated in numpy and
 checked against the oracle's restatement of the reference kernels (CPU):
 
-* partition (m <= 4): per(A) = sum over set partitions pi of the rows of
+* partition (m <= 6): per(A) = sum over set partitions pi of the rows of
   mu(pi) prod_{blocks b} p_b,  p_b = sum_j prod_{i in b} a_ij,
   mu(pi) = prod_b (-1)^(|b|-1) (|b|-1)!  -- Moebius inversion from "maps
   constant on blocks" to injective maps (the reference's combinatoric sum,
@@ -65,14 +65,15 @@ def laplace8(a):
 
 
 def test_set_partition_counts():
-    assert [sum(1 for _ in set_partitions(list(range(k)))) for k in range(1, 6)] == [1, 2, 5, 15, 52]
+    assert [sum(1 for _ in set_partitions(list(range(k)))) for k in range(1, 7)] == [1, 2, 5, 15, 52, 203]
     # |mu| summed over partitions of an m-set = m! (permutations by cycle type)
     for m in range(1, 6):
         s = sum(math.prod(math.factorial(len(b) - 1) for b in pi) for pi in set_partitions(list(range(m))))
         assert s == math.factorial(m)
 
 
-@pytest.mark.parametrize("m,n", [(1, 1), (1, 5), (2, 2), (2, 7), (3, 3), (3, 8), (4, 4), (4, 10), (4, 13)])
+@pytest.mark.parametrize("m,n", [(1, 1), (1, 5), (2, 2), (2, 7), (3, 3), (3, 8), (4, 4), (4, 10), (4, 13), (5, 7),
+                                 (5, 10), (6, 8), (6, 9)])
 def test_partition_formula_vs_oracle(m, n):
     rng = np.random.default_rng(100 * m + n)
     ai = rng.integers(-3, 4, (m, n)).astype(np.int64)
