@@ -513,3 +513,46 @@ def test_combinatoric_int128():
         P.combinatoric(huge, exact="int128")
     r = run_algorithm(as_matrix(big), AlgorithmId.COMBINATORIC, exact="int128")
     assert r.value == 2**124 + 15 and r.overflowed  # value exact, flag = does not fit int64
+
+
+def test_randomized_shapes_all_paths():
+    """Seeded fuzz over shapes, dtypes, value laws and every entry point
+    (single permanents through each algorithm and `opt`, batches through the
+    dispatch and each batch formula) against the oracle, metric (ii); integer
+    inputs bit-exact (or the reference's OverflowError on both sides)."""
+    rng = np.random.default_rng(20261020)
+    laws = [lambda s: rng.uniform(-1, 1, s), lambda s: rng.standard_normal(s), lambda s: rng.uniform(0, 1, s),
+            lambda s: (rng.random(s) < 0.3) * rng.standard_normal(s)]
+    for case in range(160):
+        n = int(rng.integers(1, 15))
+        m = int(rng.integers(1, n + 1))
+        kind = rng.choice(["f", "c", "i"], p=[0.5, 0.3, 0.2])
+        law = laws[case % len(laws)]
+        if kind == "i":
+            a = rng.integers(-3, 4, (m, n)).astype(np.int64)
+        elif kind == "c":
+            a = law((m, n)) + 1j * law((m, n))
+        else:
+            a = law((m, n))
+        ref_alg = "combinatoric" if math.perm(n, m) <= 2_000_000 else "glynn"
+        ref, ovf = O.permanent(ref_alg, a)
+        fns = [P.opt, P.glynn, P.ryser] + ([P.combinatoric] if math.perm(n, m) <= 2_000_000 else [])
+        for fn in fns:
+            if kind == "i":
+                exp = O.permanent(fn.__name__ if fn is not P.opt else ref_alg, a)
+                try:
+                    got = fn(a)
+                    assert not exp[1] and got == exp[0], (case, fn.__name__, m, n)
+                except OverflowError:
+                    assert exp[1], (case, fn.__name__, m, n)
+            else:
+                got = fn(a)
+                assert scaled_err(got, ref, magsum(a)) <= TOL, (case, fn.__name__, m, n, got, ref)
+        if kind != "i" and n <= 16:
+            B = int(rng.integers(1, 70))
+            A = np.stack([law((m, n)) + (1j * law((m, n)) if kind == "c" else 0) for _ in range(B)])
+            for bfn in (P.opt_batch, P.glynn_batch, P.ryser_batch):
+                out = bfn(A)
+                for i in (0, B - 1):
+                    r = O.permanent(ref_alg, A[i])[0]
+                    assert scaled_err(out[i], r, magsum(A[i])) <= TOL, (case, bfn.__name__, m, n, i)
