@@ -10,6 +10,7 @@
 
 #include "batch.cuh"
 #include "engine.cuh"
+#include "walk_launch.cuh"
 
 namespace permb200 {
 
@@ -132,8 +133,39 @@ static batch_fn pick_glynn_warp(int n, std::integer_sequence<int, Ns...>) {
 // the classic kernel of the same family: Laplace -> Glynn, partition ->
 // memoized combinatoric).  Thread-per-matrix needs enough matrices to fill
 // the GPU; below that a warp per matrix (n >= 9).
+// Square Glynn batches of n = 17..30: every matrix's Gray walk split into
+// segments over the grid (walk_multi_kernel), partials combined per matrix
+// in segment order inside the launch.
+static int launch_walk_multi_batch(bool cplx, int64_t B, int n, const void* dA, void* dOut, cudaStream_t stream) {
+  walk_multi_fn fn = walk_multi_lookup(cplx, n);
+  walk_multi_bps_fn bfn = walk_multi_bps_lookup(cplx, n);
+  if (!fn || !bfn) {
+    set_error("no batched walk kernel for this n");
+    return PERM_BAD_SHAPE;
+  }
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  static int bps_cache[2][kWalkMultiMaxN + 1] = {};  // benign race: idempotent
+  int& bps = bps_cache[cplx ? 1 : 0][n];
+  if (!bps) bps = bfn();
+  const WalkMultiPlan pl = plan_walk_multi(n, B, nsm, bps);
+  const size_t part_bytes = (size_t)B * pl.segs * kPartialStride * sizeof(double);
+  const size_t done_bytes = ((size_t)B * sizeof(unsigned int) + 255) & ~(size_t)255;
+  void* scratch = nullptr;
+  PERM_CUDA_TRY(cudaMallocAsync(&scratch, part_bytes + done_bytes, stream));
+  unsigned int* done = static_cast<unsigned int*>(scratch);
+  double* partials = reinterpret_cast<double*>(static_cast<char*>(scratch) + done_bytes);
+  cudaError_t e = cudaMemsetAsync(done, 0, (size_t)B * sizeof(unsigned int), stream);
+  if (e == cudaSuccess) e = fn(dA, dOut, B, partials, done, pl, stream);
+  const cudaError_t ef = cudaFreeAsync(scratch, stream);
+  if (e == cudaSuccess) e = ef;
+  return e == cudaSuccess ? PERM_OK : cuda_fail(e, "batched walk launch");
+}
+
 static int launch_batch(int alg, bool cplx, int64_t B, int m, int n, const void* dA, void* dOut,
                         cudaStream_t stream) {
+  if (alg == PERM_ALG_GLYNN && m == n && n >= kWalkMultiMinN) return launch_walk_multi_batch(cplx, B, n, dA, dOut, stream);
   if (alg == PERM_ALG_BATCH_LAPLACE || alg == PERM_ALG_BATCH_PARTITION) {
     const int st = launch_bulk_batch(alg, cplx, B, m, n, dA, dOut, stream);
     if (st >= 0) return st;
@@ -293,11 +325,11 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
     set_error(m > n ? "need m <= n; transpose first" : "bad batch shape");
     return PERM_BAD_SHAPE;
   }
-  if (n > 16) {
-    set_error("batched kernels handle n <= 16; use the single-permanent entry points");
+  if (alg < 0) alg = batch_select(m, n);
+  if (n > 16 && !(m == n && alg == PERM_ALG_GLYNN && n <= kWalkMultiMaxN)) {
+    set_error("batched kernels handle n <= 16 (square Glynn: n <= 30); use the single-permanent entry points");
     return PERM_BAD_SHAPE;
   }
-  if (alg < 0) alg = batch_select(m, n);
   if (alg > PERM_ALG_BATCH_LAPLACE) {
     set_error("unknown batch algorithm");
     return PERM_BAD_SHAPE;

@@ -492,46 +492,32 @@ __device__ __forceinline__ T walk_chunk(T (&v)[P], const T* sU, const double* sW
   return acc;
 }
 
+// Partial sums of one thread: double-double real / imaginary parts and the
+// magnitude sum.
+struct WalkAcc {
+  double hi = 0.0, lo = 0.0, hi_i = 0.0, lo_i = 0.0, mag = 0.0;
+};
+
+template <typename T, int P>
+using WalkRow0 = T[walk_r0<T, P>() ? P : 1];
+
+// The walk over warp-groups g = g_first, g_first + g_stride, ... < g_end of
+// one setup staged in shared memory (sU: B rows, sV0, this warp's seed row
+// myWarp): group g is 32 chunks of L = 2^log2L indices starting at
+// k_begin + g * 32 * L, lane l owns chunk l of the group.
 template <typename T, int P, bool W>
-__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_kernel(WalkArgs args) {
+__device__ __forceinline__ void walk_group_range(const T* sU, const T* sV0, T* myWarp, const double* sW,
+                                                 const WalkRow0<T, P>& u0, int B, int log2L, uint64_t k_begin,
+                                                 uint64_t g_first, uint64_t g_end, uint64_t g_stride, int mag_on,
+                                                 WalkAcc& A) {
   constexpr int PS = row_stride<T, P>();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sU = reinterpret_cast<T*>(smem_raw);        // [B][PS]
-  T* sV0 = sU + (size_t)args.B * PS;              // [PS]
-  T* sWarp = sV0 + PS;                            // [kWalkWarps][PS]
-  double* sW = reinterpret_cast<double*>(sWarp + kWalkWarps * PS);  // [wlen]
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int B = args.B;
-  {
-    const T* gU = static_cast<const T*>(args.U);
-    const T* gV0 = static_cast<const T*>(args.v0);
-    for (int i = tid; i < B * P; i += kWalkThreads) sU[(i / P) * PS + (i % P)] = gU[i];
-    for (int j = tid; j < P; j += kWalkThreads) sV0[j] = gV0[j];
-    if constexpr (W)
-      for (int i = tid; i < args.wlen; i += kWalkThreads) sW[i] = args.w[i];
-  }
-  __syncthreads();
-
-  const int log2L = args.log2L;
+  const int lane = threadIdx.x & 31;
   const uint64_t L = 1ull << log2L;
   const uint64_t nq = L >> 3;
   const uint64_t bmask = (B >= 64) ? ~0ull : ((1ull << B) - 1);
   const uint64_t hmask = (~0ull << (log2L + 5)) & bmask;  // warp-uniform Gray bits
-  const int mag_on = args.mag;
-  T* myWarp = sWarp + warp * PS;
-
-  double hi = 0.0, lo = 0.0, hi_i = 0.0, lo_i = 0.0, mag = 0.0;
-  const uint64_t total_warps = (uint64_t)gridDim.x * kWalkWarps;
-  T u0[walk_r0<T, P>() ? P : 1];
-  if constexpr (walk_r0<T, P>()) {
-#pragma unroll
-    for (int j = 0; j < P; ++j) u0[j] = sU[j];
-  }
-
-  for (uint64_t g = (uint64_t)blockIdx.x * kWalkWarps + warp; g < args.ngroups; g += total_warps) {
-    const uint64_t kb = args.k_begin + ((g * 32) << log2L);
+  for (uint64_t g = g_first; g < g_end; g += g_stride) {
+    const uint64_t kb = k_begin + ((g * 32) << log2L);
     const uint64_t k0 = kb + ((uint64_t)lane << log2L);
     // ---- warp-cooperative seed of the bits shared by the 32 chunks
     {
@@ -565,43 +551,157 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_ke
     const int pc = __popcll(g0);
     T acc;
     if constexpr (walk_r0<T, P>()) {
-      acc = mag_on ? walk_chunk_fused_r0<T, P, W, true>(v, u0, sU, sW, k0, nq, pc, mag)
-                   : walk_chunk_fused_r0<T, P, W, false>(v, u0, sU, sW, k0, nq, pc, mag);
+      acc = mag_on ? walk_chunk_fused_r0<T, P, W, true>(v, u0, sU, sW, k0, nq, pc, A.mag)
+                   : walk_chunk_fused_r0<T, P, W, false>(v, u0, sU, sW, k0, nq, pc, A.mag);
     } else {
-      acc = mag_on ? WALK_CHUNK<T, P, W, true>(v, sU, sW, k0, nq, pc, mag)
-                   : WALK_CHUNK<T, P, W, false>(v, sU, sW, k0, nq, pc, mag);
+      acc = mag_on ? WALK_CHUNK<T, P, W, true>(v, sU, sW, k0, nq, pc, A.mag)
+                   : WALK_CHUNK<T, P, W, false>(v, sU, sW, k0, nq, pc, A.mag);
     }
-    dd_acc(hi, lo, Num<T>::re(acc));
-    if constexpr (sizeof(T) == 16) dd_acc(hi_i, lo_i, Num<T>::im(acc));
+    dd_acc(A.hi, A.lo, Num<T>::re(acc));
+    if constexpr (sizeof(T) == 16) dd_acc(A.hi_i, A.lo_i, Num<T>::im(acc));
   }
+}
 
-  // ---- deterministic reduction: warp shuffle, then warp 0 over the block
+// Deterministic block reduction (warp shuffles, then warp leaders in order);
+// thread 0 writes {hi, lo, im_hi, im_lo, mag} to out.
+template <bool CPLX>
+__device__ __forceinline__ void walk_block_reduce(WalkAcc A, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    double h2 = __shfl_down_sync(0xffffffffu, hi, off), l2 = __shfl_down_sync(0xffffffffu, lo, off);
-    dd_add(hi, lo, h2, l2);
-    if constexpr (sizeof(T) == 16) {
-      double h3 = __shfl_down_sync(0xffffffffu, hi_i, off), l3 = __shfl_down_sync(0xffffffffu, lo_i, off);
-      dd_add(hi_i, lo_i, h3, l3);
+    double h2 = __shfl_down_sync(0xffffffffu, A.hi, off), l2 = __shfl_down_sync(0xffffffffu, A.lo, off);
+    dd_add(A.hi, A.lo, h2, l2);
+    if constexpr (CPLX) {
+      double h3 = __shfl_down_sync(0xffffffffu, A.hi_i, off), l3 = __shfl_down_sync(0xffffffffu, A.lo_i, off);
+      dd_add(A.hi_i, A.lo_i, h3, l3);
     }
-    mag += __shfl_down_sync(0xffffffffu, mag, off);
+    A.mag += __shfl_down_sync(0xffffffffu, A.mag, off);
   }
   __shared__ double red[kWalkWarps][5];
   if (lane == 0) {
-    red[warp][0] = hi; red[warp][1] = lo; red[warp][2] = hi_i; red[warp][3] = lo_i; red[warp][4] = mag;
+    red[warp][0] = A.hi; red[warp][1] = A.lo; red[warp][2] = A.hi_i; red[warp][3] = A.lo_i; red[warp][4] = A.mag;
   }
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     double H = red[0][0], Lo = red[0][1], Hi2 = red[0][2], Lo2 = red[0][3], M = red[0][4];
     for (int w = 1; w < kWalkWarps; ++w) {
       dd_add(H, Lo, red[w][0], red[w][1]);
       dd_add(Hi2, Lo2, red[w][2], red[w][3]);
       M += red[w][4];
     }
-    double* out = args.partials + (size_t)blockIdx.x * kPartialStride;
     out[0] = H; out[1] = Lo; out[2] = Hi2; out[3] = Lo2; out[4] = M;
   }
+}
+
+template <typename T, int P, bool W>
+__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_kernel(WalkArgs args) {
+  constexpr int PS = row_stride<T, P>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sU = reinterpret_cast<T*>(smem_raw);        // [B][PS]
+  T* sV0 = sU + (size_t)args.B * PS;              // [PS]
+  T* sWarp = sV0 + PS;                            // [kWalkWarps][PS]
+  double* sW = reinterpret_cast<double*>(sWarp + kWalkWarps * PS);  // [wlen]
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int B = args.B;
+  {
+    const T* gU = static_cast<const T*>(args.U);
+    const T* gV0 = static_cast<const T*>(args.v0);
+    for (int i = tid; i < B * P; i += kWalkThreads) sU[(i / P) * PS + (i % P)] = gU[i];
+    for (int j = tid; j < P; j += kWalkThreads) sV0[j] = gV0[j];
+    if constexpr (W)
+      for (int i = tid; i < args.wlen; i += kWalkThreads) sW[i] = args.w[i];
+  }
+  __syncthreads();
+
+  WalkRow0<T, P> u0;
+  if constexpr (walk_r0<T, P>()) {
+#pragma unroll
+    for (int j = 0; j < P; ++j) u0[j] = sU[j];
+  }
+  WalkAcc A;
+  walk_group_range<T, P, W>(sU, sV0, sWarp + warp * PS, sW, u0, B, args.log2L, args.k_begin,
+                            (uint64_t)blockIdx.x * kWalkWarps + warp, args.ngroups,
+                            (uint64_t)gridDim.x * kWalkWarps, args.mag, A);
+  walk_block_reduce<sizeof(T) == 16>(A, args.partials + (size_t)blockIdx.x * kPartialStride);
   walk_last_block_combine(args.partials, args.final_out, args.done);
+}
+
+// Many square Glynn permanents in one launch (batches of n = 17..30): work
+// item w = (matrix w / segs, segment w % segs); each block builds its
+// matrix's walk setup (v0 = column sums, U[t] = -2 row(n-1-t)) in shared
+// memory straight from the [B][n][n] batch, walks its segment's groups,
+// writes a block partial, and the last segment of a matrix to finish
+// (per-matrix counter) combines its segments in order -> out[matrix].
+struct WalkMultiArgs {
+  const void* a;          // [nmats][P][P] row-major, device
+  void* out;              // [nmats] permanents
+  double* partials;       // [nmats * segs][kPartialStride]
+  unsigned int* done;     // [nmats], zero on entry, reset on exit
+  int64_t nmats;
+  int segs, log2L;
+  uint64_t groups_per_seg;
+  double scale;           // 2^-(n-1)
+};
+
+template <typename T, int P>
+__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_multi_kernel(WalkMultiArgs args) {
+  constexpr int PS = row_stride<T, P>();
+  constexpr int B = P - 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sU = reinterpret_cast<T*>(smem_raw);  // [B][PS]
+  T* sV0 = sU + (size_t)B * PS;             // [PS]
+  T* sWarp = sV0 + PS;                      // [kWalkWarps][PS]
+  __shared__ bool last;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int64_t items = args.nmats * args.segs;
+  for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+    const int64_t mat = w / args.segs;
+    const int seg = (int)(w - mat * args.segs);
+    const T* A = static_cast<const T*>(args.a) + mat * P * P;
+    __syncthreads();  // previous item's shared memory is free
+    for (int i = tid; i < B * P; i += kWalkThreads) {
+      const int t = i / P, j = i - t * P;
+      sU[t * PS + j] = Num<T>::scale(-2.0, A[(P - 1 - t) * P + j]);
+    }
+    for (int j = tid; j < P; j += kWalkThreads) {
+      T c = A[j];
+      for (int i = 1; i < P; ++i) c = Num<T>::add(c, A[i * P + j]);
+      sV0[j] = c;
+    }
+    __syncthreads();
+    WalkRow0<T, P> u0;
+    if constexpr (walk_r0<T, P>()) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) u0[j] = sU[j];
+    }
+    WalkAcc acc;
+    const uint64_t g0 = (uint64_t)seg * args.groups_per_seg;
+    walk_group_range<T, P, false>(sU, sV0, sWarp + warp * PS, nullptr, u0, B, args.log2L, 0, g0 + warp,
+                                  g0 + args.groups_per_seg, kWalkWarps, 0, acc);
+    double* part = args.partials + (size_t)w * kPartialStride;
+    walk_block_reduce<sizeof(T) == 16>(acc, part);
+    if (tid == 0) {
+      __threadfence();
+      last = (atomicAdd(&args.done[mat], 1u) == (unsigned)args.segs - 1);
+    }
+    __syncthreads();
+    if (last && tid == 0) {
+      __threadfence();
+      const volatile double* p = args.partials + (size_t)mat * args.segs * kPartialStride;
+      double H = p[0], Lo = p[1], H2 = p[2], L2 = p[3];
+      for (int s = 1; s < args.segs; ++s) {
+        dd_add(H, Lo, p[s * kPartialStride], p[s * kPartialStride + 1]);
+        dd_add(H2, L2, p[s * kPartialStride + 2], p[s * kPartialStride + 3]);
+      }
+      T r;
+      if constexpr (sizeof(T) == 16) r = cd_make((H + Lo) * args.scale, (H2 + L2) * args.scale);
+      else r = (H + Lo) * args.scale;
+      static_cast<T*>(args.out)[mat] = r;
+      args.done[mat] = 0u;
+    }
+  }
 }
 
 // Single-thread walk for tiny index spaces (< 32 chunks of 8): runtime P.

@@ -2,6 +2,7 @@
 #pragma once
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdlib>
 #include <utility>
 
@@ -145,6 +146,68 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
   kern<<<(unsigned)grid, kWalkThreads, smem, stream>>>(a);
   return cudaGetLastError();
 }
+
+// ---- many square Glynn walks in one launch (batches of n = 17..30) -------
+struct WalkMultiPlan {
+  int segs = 1, log2L = 3;
+  uint64_t groups_per_seg = 0;
+  int grid = 0;
+};
+// Segments per matrix: work items (matrix, segment) are dealt round-robin to
+// a grid of at most 8 blocks per resident slot, so the last wave's fill
+// decides the efficiency; split each matrix until there are >= 8 waves of
+// items, keeping >= 8 groups of 32 chunks of L >= 2^8 per segment (one group
+// per warp).  Chunk length as long as the segment allows, capped like
+// single walks.
+inline WalkMultiPlan plan_walk_multi(int n, int64_t nmats, int nsm, int bps) {
+  WalkMultiPlan pl;
+  const int bits = n - 1;  // log2 of the steps per matrix
+  const int64_t slots = (int64_t)nsm * bps;
+  int lseg = 0;
+  while ((nmats << lseg) < 8 * slots && bits - 8 - (lseg + 1) >= 8) ++lseg;
+  pl.segs = 1 << lseg;
+  pl.log2L = std::min(walk_max_log2L(), bits - 8 - lseg);  // 8 warps x 32 lanes x L per segment pass
+  if (pl.log2L < 3) pl.log2L = 3;
+  pl.groups_per_seg = ((1ull << bits) >> (pl.log2L + 5)) >> lseg;
+  const int64_t items = nmats * pl.segs;
+  pl.grid = (int)std::min<int64_t>(items, slots * 8);
+  return pl;
+}
+
+template <typename T, int P>
+cudaError_t launch_walk_multi(const void* a, void* out, int64_t nmats, double* partials, unsigned int* done,
+                              const WalkMultiPlan& pl, cudaStream_t stream) {
+  constexpr int PS = row_stride<T, P>();
+  const size_t smem = (size_t)((P - 1) * PS + PS + kWalkWarps * PS) * sizeof(T);
+  WalkMultiArgs args;
+  args.a = a;
+  args.out = out;
+  args.partials = partials;
+  args.done = done;
+  args.nmats = nmats;
+  args.segs = pl.segs;
+  args.log2L = pl.log2L;
+  args.groups_per_seg = pl.groups_per_seg;
+  args.scale = std::ldexp(1.0, -(P - 1));
+  walk_multi_kernel<T, P><<<pl.grid, kWalkThreads, smem, stream>>>(args);
+  return cudaGetLastError();
+}
+template <typename T, int P>
+int walk_multi_blocks_per_sm() {
+  constexpr int PS = row_stride<T, P>();
+  const size_t smem = (size_t)((P - 1) * PS + PS + kWalkWarps * PS) * sizeof(T);
+  int bps = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_multi_kernel<T, P>, kWalkThreads, smem) != cudaSuccess)
+    bps = 1;
+  return bps < 1 ? 1 : bps;
+}
+using walk_multi_fn = cudaError_t (*)(const void*, void*, int64_t, double*, unsigned int*, const WalkMultiPlan&,
+                                      cudaStream_t);
+using walk_multi_bps_fn = int (*)();
+// walk_multi_inst.cu: P = 17..30, double and cd
+walk_multi_fn walk_multi_lookup(bool cplx, int P);
+walk_multi_bps_fn walk_multi_bps_lookup(bool cplx, int P);
+constexpr int kWalkMultiMinN = 17, kWalkMultiMaxN = 30;
 
 template <typename T, bool W, int... Ps>
 walk_fn walk_pick(int P, std::integer_sequence<int, Ps...>) {

@@ -398,6 +398,32 @@ def test_laplace_batch_8x8():
         assert scaled_err(outc[i], ref, magsum(Cx[i])) <= TOL
 
 
+@pytest.mark.parametrize("cplx", [False, True])
+def test_batched_medium_walks(cplx):
+    """Square Glynn batches of n = 17..30 (one launch, segments per matrix):
+    every result equals the single-matrix engine's within metric (ii), and
+    matches the oracle's double-double walk for n <= 20; batch sizes from 1
+    (many segments per matrix) to a few hundred (one segment each)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(1717 + cplx)
+    for n, B in ((17, 1), (17, 300), (18, 7), (20, 64), (22, 3), (24, 20), (26, 2), (30, 1)):
+        A = rng.uniform(-1, 1, (B, n, n)) / n
+        if cplx:
+            A = A + 1j * rng.uniform(-1, 1, (B, n, n)) / n
+        out = P.glynn_batch(A)
+        assert np.array_equal(out, P.opt_batch(A))
+        dev = P.glynn_batch(torch.tensor(A, device="cuda")).cpu().numpy()
+        assert np.array_equal(out, dev)
+        for i in sorted({0, B // 2, B - 1}):
+            v, M = P.permanent_with_magsum(as_matrix(A[i]), AlgorithmId.GLYNN)
+            assert scaled_err(out[i], v, M) <= TOL, (n, B, i)
+            if n <= 20:
+                ref = O.dd_permanent("glynn", A[i], nthreads=8)
+                assert scaled_err(out[i], ref, M) <= TOL, (n, B, i)
+    with pytest.raises(ValueError):
+        P.ryser_batch(rng.uniform(-1, 1, (2, 17, 17)))  # other algorithms stop at n = 16
+
+
 def _dd_value(a, alg):
     from paper_2510_03421_b200 import engine as E
 
