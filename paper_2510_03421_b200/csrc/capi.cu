@@ -24,6 +24,7 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
 int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a, double* out, int dev_ptr,
                     void* stream);
 int batch_select(int m, int n);
+int tiny_permanent(int alg, bool cplx, int m, int n, const double* a, double* out);
 int dd_permanent(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out4,
                  void* stream);
 int int_walk_partial(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, uint64_t k0,
@@ -76,8 +77,13 @@ int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, 
     return comb_permanent(true, cplx ? 1 : 0, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream_);
   // walks shorter than one warp-group of chunks (Glynn n <= 8, Ryser n <= 7):
   // the register-resident thread-per-matrix batch kernels, batch of one
-  if (magsum == nullptr && !dev_ptr && lda == n && walk_steps(alg, m, n) < 256)
+  if (magsum == nullptr && !dev_ptr && lda == n && walk_steps(alg, m, n) < 256) {
+    if (stream_ == nullptr) {  // zero-copy round trip (mapped pinned memory, flag spin)
+      const int tst = tiny_permanent(alg, cplx, m, n, a, out);
+      if (tst >= 0) return tst;
+    }
     return batch_permanent(alg, cplx, 1, m, n, a, out, 0, stream_);
+  }
   cudaStream_t stream = pick_stream(stream_);
   HostMat A;
   st = load_matrix(m, n, a, lda, dev_ptr, cplx, &A, stream);

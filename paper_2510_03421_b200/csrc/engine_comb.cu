@@ -167,6 +167,8 @@ static void combine_float(const std::vector<int64_t>& h, double* re_h, double* r
 // Float: out[0..1] = re, im.  Mode 2: *ivalue, PERM_OVERFLOW on reference
 // overflow.  Mode 3: ivalue[0..1] = lo, hi; PERM_OVERFLOW when the a-priori
 // bound (product of the row sums of |A|) does not certify int128.
+int tiny_permanent(int alg, bool cplx, int m, int n, const double* a, double* out);  // engine_batch.cu
+
 int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t lda, int dev_ptr,
                    uint64_t step_budget, double* out, int64_t* ivalue, void* stream_) {
   clear_error();
@@ -188,6 +190,13 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
   if (mode == 3 && ryser) {
     set_error("exact int128 combination-order Ryser is not provided; use the int128 walk");
     return PERM_BAD_ARG;
+  }
+  // tiny float combinatoric from host memory: the zero-copy batch-of-one path
+  // (memoized-DP kernel, m <= 4; the generic thread-per-matrix DFS is slower
+  // than the tree-split comb kernel below from 5x5 on)
+  if (!ryser && mode <= 1 && !dev_ptr && lda == n && stream_ == nullptr && m <= 4 && n <= 12) {
+    const int tst = tiny_permanent(PERM_ALG_COMBINATORIC, mode == 1, m, n, static_cast<const double*>(a), out);
+    if (tst >= 0) return tst;
   }
   cudaStream_t stream = pick_stream(stream_);
   const int esz = (mode == 1) ? 16 : 8;
