@@ -25,6 +25,13 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
                     void* stream);
 int batch_select(int m, int n);
 int tiny_permanent(int alg, bool cplx, int m, int n, const double* a, double* out);
+static int tiny_glynn_max_n() {
+  static const int v = [] {
+    const char* e = std::getenv("PERM_TINY_GLYNN_MAX_N");
+    return (e && *e) ? std::atoi(e) : 12;
+  }();
+  return v;
+}
 int dd_permanent(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out4,
                  void* stream);
 int int_walk_partial(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, uint64_t k0,
@@ -83,6 +90,14 @@ int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, 
       if (tst >= 0) return tst;
     }
     return batch_permanent(alg, cplx, 1, m, n, a, out, 0, stream_);
+  }
+  // square Glynn n = 9..TINY_GLYNN_MAX_N: one warp walks the matrix (the
+  // warp-per-matrix batch kernel) on the zero-copy path, cheaper than a
+  // device-wide walk launch at these sizes
+  if (magsum == nullptr && !dev_ptr && lda == n && stream_ == nullptr && alg == PERM_ALG_GLYNN && m == n &&
+      n <= tiny_glynn_max_n()) {
+    const int tst = tiny_permanent(alg, cplx, m, n, a, out);
+    if (tst >= 0) return tst;
   }
   cudaStream_t stream = pick_stream(stream_);
   HostMat A;
