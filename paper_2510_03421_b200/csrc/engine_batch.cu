@@ -339,7 +339,7 @@ struct TinyBuf {
   char* dev = nullptr;   // device alias of host
   cudaStream_t stream = nullptr;
   unsigned int seq = 0;
-  static constexpr size_t kIn = 16 * 1024, kOut = 64;
+  static constexpr size_t kIn = 256 * 1024, kOut = 32 * 1024;
   int ensure() {
     int d = 0;
     cudaGetDevice(&d);
@@ -361,6 +361,41 @@ static bool tiny_enabled() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+
+// launch the batch kernel on the mapped buffers, publish a sequence number,
+// spin until it lands (blocking wait after 2 ms, which also reports errors)
+static int tiny_run(TinyBuf& tb, int alg, bool cplx, int64_t B, int m, int n) {
+  int st = launch_batch(alg, cplx, B, m, n, tb.dev, tb.dev + TinyBuf::kIn, tb.stream);
+  if (st != PERM_OK) return st;
+  const unsigned int seq = ++tb.seq;
+  volatile unsigned int* hflag = reinterpret_cast<volatile unsigned int*>(tb.host + TinyBuf::kIn + TinyBuf::kOut);
+  tiny_flag_kernel<<<1, 1, 0, tb.stream>>>(
+      reinterpret_cast<volatile unsigned int*>(tb.dev + TinyBuf::kIn + TinyBuf::kOut), seq);
+  PERM_CUDA_TRY(cudaGetLastError());
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*hflag != seq) {
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) {
+      PERM_CUDA_TRY(cudaStreamSynchronize(tb.stream));
+      break;
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  return PERM_OK;
+}
+
+// A whole small host batch through the mapped buffers (C1: 64 x 12x12).
+static int tiny_batch_host(int alg, bool cplx, int64_t B, int m, int n, const double* a, double* out) {
+  const size_t esz = cplx ? 16 : 8;
+  const size_t in_b = (size_t)B * m * n * esz, out_b = (size_t)B * esz;
+  if (!tiny_enabled() || in_b > TinyBuf::kIn || out_b > TinyBuf::kOut) return -1;
+  TinyBuf& tb = g_tiny;
+  if (tb.ensure() != PERM_OK) return -1;
+  std::memcpy(tb.host, a, in_b);
+  const int st = tiny_run(tb, alg, cplx, B, m, n);
+  if (st != PERM_OK) return st;
+  std::memcpy(out, tb.host + TinyBuf::kIn, out_b);
+  return PERM_OK;
 }
 
 // -1: not taken (caller uses the staged path)
@@ -396,23 +431,8 @@ int tiny_permanent(int alg, bool cplx, int m, int n, const double* a, double* ou
   } else {
     std::memcpy(tb.host, a, bytes);
   }
-  int st = launch_batch(alg, cplx, 1, pad ? n : m, n, tb.dev, tb.dev + TinyBuf::kIn, tb.stream);
+  const int st = tiny_run(tb, alg, cplx, 1, pad ? n : m, n);
   if (st != PERM_OK) return st;
-  const unsigned int seq = ++tb.seq;
-  volatile unsigned int* hflag = reinterpret_cast<volatile unsigned int*>(tb.host + TinyBuf::kIn + TinyBuf::kOut);
-  tiny_flag_kernel<<<1, 1, 0, tb.stream>>>(
-      reinterpret_cast<volatile unsigned int*>(tb.dev + TinyBuf::kIn + TinyBuf::kOut), seq);
-  PERM_CUDA_TRY(cudaGetLastError());
-  // spin briefly on the flag; fall back to a blocking wait (and its error
-  // report) if the kernel has not signalled after ~2 ms
-  const auto t0 = std::chrono::steady_clock::now();
-  while (*hflag != seq) {
-    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) {
-      PERM_CUDA_TRY(cudaStreamSynchronize(tb.stream));
-      break;
-    }
-  }
-  std::atomic_thread_fence(std::memory_order_acquire);
   std::memcpy(out, tb.host + TinyBuf::kIn, esz);
   if (pad) {
     out[0] *= unscale;
@@ -460,6 +480,10 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
   const size_t esz = cplx ? 16 : 8;
   const size_t mat_bytes = (size_t)m * n * esz;
   if (dev_ptr) return launch_batch(alg, cplx, B, m, n, a, out, stream);
+  if (stream_ == nullptr) {  // small host batches: zero-copy round trip
+    const int tst = tiny_batch_host(alg, cplx, B, m, n, a, out);
+    if (tst >= 0) return tst;
+  }
   // Host arrays: chunked pipeline through two pinned staging slots on two
   // engine streams, so the host copy of chunk c+1, the H2D DMA of chunk c and
   // the kernels overlap (the input is read from pageable numpy memory).
