@@ -20,7 +20,7 @@
 //
 // Formulas (cheaper per matrix than any reference algorithm, exact algebra):
 //
-//  * Rectangular m <= 4 (C2b 4x10): the Moebius inversion over set partitions
+//  * Rectangular m <= 6 (C2b 4x10): the Moebius inversion over set partitions
 //    of the rows (sum over injective row->column maps =
 //    sum_pi mu(pi) prod_{blocks b} p_b,  p_b = sum_j prod_{i in b} a_ij,
 //    mu(pi) = prod_b (-1)^(|b|-1) (|b|-1)!):  m = 4 costs (2^m-1-m) muls +
@@ -31,9 +31,9 @@
 //    per = sum_{|X|=4} per(A[0:4, X]) per(A[4:8, X^c]), with the 4x4 minors
 //    built from 2x2 row-pair permanents q(P):
 //      per(A[0:4, X]) = sum_{P subset X, |P|=2} q01(P) q23(X \ P).
-//    A lane pair owns one matrix: lane 2j the top half, lane 2j+1 the bottom;
-//    each forms its 2 x 28 q-tables and 70 minors, the pair exchanges minors
-//    by warp shuffle.  1204 flops per matrix against 2048 for Glynn.
+//    A thread owns one matrix: its 4 x 28 q-tables, the top half's 70 minors
+//    parked in shared memory, the bottom half's 70 minors on the complements.
+//    1134 flops per matrix against 2048 for Glynn.
 #pragma once
 #include <utility>
 #include "common.cuh"
@@ -394,18 +394,9 @@ __host__ __device__ constexpr LpSub lp_sub(int p) {
 // per(H[:, {a,b,c,d}]) of a 4-row half H from its row-pair tables qa (rows
 // 0,1) and qb (rows 2,3) is the sum over the 6 ordered splits of {a,b,c,d}
 // into two pairs, qa(pair) * qb(other pair): one DMUL + five DFMAs.
-// Half exchange: the top lane accumulates pairs 0..17, the bottom lane pairs
-// 18..34; at step i each lane sends the partner the two minors the partner
-// needs (selected by lane half), so every 32-bit shuffle carries useful data
-// both ways: 70 SHFL per lane instead of 140, 35 products instead of 70.
-//
-// Scheduling: B200's FP64 pipe only reaches its peak when each warp issues
-// long runs of independent DFMAs (tools/fp64_occ_probe.cu: a dependency
-// every 4 / 8 / 16 instructions gives 73 / 86 / 98% of the pipe, whatever
-// the occupancy), so the minors of GI steps (4*GI of them) are built term by
-// term across all of them -- a dependency distance of 4*GI instructions.
-//
-// minor slot m of step i: m = 0, 1 -> pair i (X, X^c); m = 2, 3 -> pair i+18
+// Term s (0..5, the ordered splits (ab|cd) (cd|ab) (ac|bd) (bd|ac) (ad|bc)
+// (bc|ad)) of minor slot (pair, side) of the 35 (X, X^c) pairs: the index of
+// its qa (which = 0) or qb (which = 1) factor.
 __host__ __device__ constexpr int lp_term(int pair, int side, int s, int which) {
   const LpSub q = lp_sub(pair);
   const int a = side ? q.c[0] : q.x[0], b = side ? q.c[1] : q.x[1];
@@ -415,53 +406,6 @@ __host__ __device__ constexpr int lp_term(int pair, int side, int s, int which) 
   const int p1[6][2] = {{c, d}, {a, b}, {b, d}, {a, c}, {b, c}, {a, d}};
   return which == 0 ? lp_pidx(p0[s][0], p0[s][1]) : lp_pidx(p1[s][0], p1[s][1]);
 }
-template <int I0, int S, int... Ms>
-__device__ __forceinline__ void lp_wide_term(const double (&qa)[28], const double (&qb)[28], double (&g)[sizeof...(Ms)],
-                                             std::integer_sequence<int, Ms...>) {
-  // slot Ms: step I0 + Ms/4, pair (Ms%4 < 2 ? step : step+18), side Ms%2
-  if constexpr (S == 0) {
-    ((g[Ms] = (((Ms & 3) < 2) || (I0 + Ms / 4 + 18 < 35))
-                  ? qa[lp_term(((Ms & 3) < 2) ? I0 + Ms / 4 : (I0 + Ms / 4 + 18) % 35, Ms & 1, 0, 0)] *
-                        qb[lp_term(((Ms & 3) < 2) ? I0 + Ms / 4 : (I0 + Ms / 4 + 18) % 35, Ms & 1, 0, 1)]
-                  : 0.0),
-     ...);
-  } else {
-    ((g[Ms] = (((Ms & 3) < 2) || (I0 + Ms / 4 + 18 < 35))
-                  ? fma(qa[lp_term(((Ms & 3) < 2) ? I0 + Ms / 4 : (I0 + Ms / 4 + 18) % 35, Ms & 1, S, 0)],
-                        qb[lp_term(((Ms & 3) < 2) ? I0 + Ms / 4 : (I0 + Ms / 4 + 18) % 35, Ms & 1, S, 1)], g[Ms])
-                  : 0.0),
-     ...);
-  }
-}
-template <int I0, int GI>
-__device__ __forceinline__ void lp_wide_group(const double (&qa)[28], const double (&qb)[28], bool bottom,
-                                              double (&acc)[8]) {
-  double g[4 * GI];
-  using Seq = std::make_integer_sequence<int, 4 * GI>;
-  lp_wide_term<I0, 0>(qa, qb, g, Seq{});
-  lp_wide_term<I0, 1>(qa, qb, g, Seq{});
-  lp_wide_term<I0, 2>(qa, qb, g, Seq{});
-  lp_wide_term<I0, 3>(qa, qb, g, Seq{});
-  lp_wide_term<I0, 4>(qa, qb, g, Seq{});
-  lp_wide_term<I0, 5>(qa, qb, g, Seq{});
-  double r[2 * GI];
-#pragma unroll
-  for (int i = 0; i < GI; ++i) {
-    r[2 * i] = __shfl_xor_sync(0xffffffffu, bottom ? g[4 * i] : g[4 * i + 2], 1);
-    r[2 * i + 1] = __shfl_xor_sync(0xffffffffu, bottom ? g[4 * i + 1] : g[4 * i + 3], 1);
-  }
-#pragma unroll
-  for (int i = 0; i < GI; ++i) {
-    const double o0 = bottom ? g[4 * i + 2] : g[4 * i], o1 = bottom ? g[4 * i + 3] : g[4 * i + 1];
-    acc[(2 * i) & 7] = fma(o0, r[2 * i + 1], acc[(2 * i) & 7]);
-    acc[(2 * i + 1) & 7] = fma(o1, r[2 * i], acc[(2 * i + 1) & 7]);
-  }
-}
-template <int GI, int... Ks>
-__device__ __forceinline__ void lp_wide_all(const double (&qa)[28], const double (&qb)[28], bool bottom,
-                                            double (&acc)[8], std::integer_sequence<int, Ks...>) {
-  (lp_wide_group<Ks * GI, (18 - Ks * GI < GI) ? 18 - Ks * GI : GI>(qa, qb, bottom, acc), ...);
-}
 // 2x2 row-pair permanents of the 8 logical columns held as 16 doubles (row r0 = v[0..7], r1 = v[8..15])
 __device__ __forceinline__ void lp_qtable(const double (&v)[16], double (&q)[28]) {
 #pragma unroll
@@ -470,51 +414,105 @@ __device__ __forceinline__ void lp_qtable(const double (&v)[16], double (&q)[28]
     for (int k = i + 1; k < 8; ++k) q[lp_pidx(i, k)] = fma(v[i], v[8 + k], v[k] * v[8 + i]);
 }
 
-template <int G>
-struct Laplace8OpT {
-  static constexpr int kLanes = 2;
+
+// Thread per matrix: the top half's 70 minors go to the thread's column of a
+// shared-memory buffer (conflict-free: consecutive threads, consecutive
+// words), then the bottom half's minors on the complements consume them --
+// no shuffles or selects.  Minors are built G at a time, term-major, so each
+// warp issues runs of G independent DFMAs.  The matrix is read with a
+// lane-dependent column rotation (pairs of columns, rho) and a swap of the
+// two rows of each 128-byte row (t): per is invariant under both, and every
+// LDS.128 of a warp is 4 wavefronts.
+template <int TPB, int G>
+struct Laplace8TOp {
+  static constexpr int kLanes = 1;
+  // term T of minor slot X (X = 2*pair + side; FLIP: the complement's minor)
+  template <int T, int FLIP, int X0, int... Ms>
+  __device__ __forceinline__ static void term(const double (&qa)[28], const double (&qb)[28], double (&g)[sizeof...(Ms)],
+                                              std::integer_sequence<int, Ms...>) {
+    if constexpr (T == 0) {
+      ((g[Ms] = qa[lp_term((X0 + Ms) >> 1, ((X0 + Ms) & 1) ^ FLIP, 0, 0)] *
+                qb[lp_term((X0 + Ms) >> 1, ((X0 + Ms) & 1) ^ FLIP, 0, 1)]),
+       ...);
+    } else {
+      ((g[Ms] = fma(qa[lp_term((X0 + Ms) >> 1, ((X0 + Ms) & 1) ^ FLIP, T, 0)],
+                    qb[lp_term((X0 + Ms) >> 1, ((X0 + Ms) & 1) ^ FLIP, T, 1)], g[Ms])),
+       ...);
+    }
+  }
+  template <int FLIP, int X0, int... Ms>
+  __device__ __forceinline__ static void minors(const double (&qa)[28], const double (&qb)[28],
+                                                double (&g)[sizeof...(Ms)], std::integer_sequence<int, Ms...> seq) {
+    term<0, FLIP, X0>(qa, qb, g, seq);
+    term<1, FLIP, X0>(qa, qb, g, seq);
+    term<2, FLIP, X0>(qa, qb, g, seq);
+    term<3, FLIP, X0>(qa, qb, g, seq);
+    term<4, FLIP, X0>(qa, qb, g, seq);
+    term<5, FLIP, X0>(qa, qb, g, seq);
+  }
+  template <int X0, int... Ms>
+  __device__ __forceinline__ static void minors_store(const double (&qa)[28], const double (&qb)[28], double* gcol,
+                                                      std::integer_sequence<int, Ms...> seq) {
+    double g[sizeof...(Ms)];
+    minors<0, X0>(qa, qb, g, seq);
+    ((gcol[(X0 + Ms) * TPB] = g[Ms]), ...);
+  }
+  template <int X0, int... Ms>
+  __device__ __forceinline__ static void minors_use(const double (&qc)[28], const double (&qd)[28], const double* gcol,
+                                                    double (&acc)[8], std::integer_sequence<int, Ms...> seq) {
+    double h[sizeof...(Ms)];
+    minors<1, X0>(qc, qd, h, seq);
+    ((acc[Ms & 7] = fma(gcol[(X0 + Ms) * TPB], h[Ms], acc[Ms & 7])), ...);
+  }
+  template <int... Ks>
+  __device__ __forceinline__ static void all_store(const double (&qa)[28], const double (&qb)[28], double* gcol,
+                                                   std::integer_sequence<int, Ks...>) {
+    (minors_store<Ks * G>(qa, qb, gcol, std::make_integer_sequence<int, (70 - Ks * G < G) ? 70 - Ks * G : G>{}), ...);
+  }
+  template <int... Ks>
+  __device__ __forceinline__ static void all_use(const double (&qc)[28], const double (&qd)[28], const double* gcol,
+                                                 double (&acc)[8], std::integer_sequence<int, Ks...>) {
+    (minors_use<Ks * G>(qc, qd, gcol, acc, std::make_integer_sequence<int, (70 - Ks * G < G) ? 70 - Ks * G : G>{}),
+     ...);
+  }
+  __device__ __forceinline__ static void load_q(const double2* H, int rho, int t, double (&q)[28]) {
+    double v[16];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double2 x = H[(((c & 3) + rho) & 3) | (((c >> 2) ^ t) << 2)];
+      v[(c >> 2) * 8 + 2 * (c & 3)] = x.x;
+      v[(c >> 2) * 8 + 2 * (c & 3) + 1] = x.y;
+    }
+    lp_qtable(v, q);
+  }
   template <class R>
   __device__ __forceinline__ static void run(const double* tile, int64_t first, int cnt, double* out, int me,
                                              R&& release) {
-    const int lane = me & 31, warp = me >> 5;
-    const int jj = lane >> 1, half = lane & 1;
-    const int mat = warp * 16 + jj;
-    // this lane's 4 rows: two 128-byte rows of 8 16-byte chunks (2 matrix rows each)
-    const double2* H = reinterpret_cast<const double2*>(tile + (size_t)mat * 64 + half * 32);
-    // logical chunk c -> physical chunk: column pairs rotated by rho, the two
-    // matrix rows of a 128-byte row swapped when t (both are symmetries of
-    // the q-tables; the pair's two lanes share rho so X / X^c line up)
-    const int rho = jj & 3, t = (jj >> 2) & 1;
-    double qa[28], qb[28];
+    __shared__ double gbuf[70 * TPB];
+    const int lane = me & 31;
+    const int rho = lane & 3, t = (lane >> 2) & 1;
+    const double2* M = reinterpret_cast<const double2*>(tile + (size_t)me * 64);
+    double* gcol = gbuf + me;
     {
-      double v[16];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const double2 x = H[(((c & 3) + rho) & 3) | (((c >> 2) ^ t) << 2)];
-        v[(c >> 2) * 8 + 2 * (c & 3)] = x.x;
-        v[(c >> 2) * 8 + 2 * (c & 3) + 1] = x.y;
-      }
-      lp_qtable(v, qa);
+      double qa[28], qb[28];
+      load_q(M, rho, t, qa);
+      load_q(M + 8, rho, t, qb);
+      all_store(qa, qb, gcol, std::make_integer_sequence<int, (70 + G - 1) / G>{});
     }
-    {
-      double v[16];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const double2 x = H[8 + ((((c & 3) + rho) & 3) | (((c >> 2) ^ t) << 2))];
-        v[(c >> 2) * 8 + 2 * (c & 3)] = x.x;
-        v[(c >> 2) * 8 + 2 * (c & 3) + 1] = x.y;
-      }
-      lp_qtable(v, qb);
-    }
-    release();  // the tables are all this lane needs: free the slot before the minors
+    double qc[28], qd[28];
+    load_q(M + 16, rho, t, qc);
+    load_q(M + 24, rho, t, qd);
+    release();
     double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    lp_wide_all<G>(qa, qb, half != 0, acc, std::make_integer_sequence<int, (18 + G - 1) / G>{});
-    const double mine = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-    const double other = __shfl_xor_sync(0xffffffffu, mine, 1);
-    if (half == 0 && mat < cnt) out[first + mat] = mine + other;
+    all_use(qc, qd, gcol, acc, std::make_integer_sequence<int, (70 + G - 1) / G>{});
+    const double r = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    if (me < cnt) out[first + me] = r;
   }
 };
 
-using Laplace8Op = Laplace8OpT<4>;  // 4 steps = 16 minors per group
+  // 4 steps = 16 minors per group
+
+// 32 threads (matrices) per block, 7 minors per group: C2a 0.115 ms
+using Laplace8Op = Laplace8TOp<32, 7>;
 
 }  // namespace permb200

@@ -61,10 +61,11 @@ cudaError_t launch_partition(const void* a, void* out, int64_t B, cudaStream_t s
   return cudaGetLastError();
 }
 
-// Laplace 8x8: 64 threads (32 matrices) per block, three stages, four blocks
-// per SM (240 registers; C2a 1e6 x 8x8: 0.122 ms against 0.184 ms for the
-// thread-per-matrix Glynn kernel, tools/bulk_bench.cu).
-constexpr int kLapTPB = 64, kLapStages = 3, kLapPerSM = 4;
+// Laplace 8x8: 32 threads (matrices) per block, two stages, four blocks per
+// SM (240 registers, 18 KB of minors per block; C2a 1e6 x 8x8: 0.115 ms
+// against 0.184 ms for the thread-per-matrix Glynn kernel and 0.124 ms for a
+// lane-pair variant with shuffles, tools/bulk_bench.cu).
+constexpr int kLapTPB = 32, kLapStages = 2, kLapPerSM = 4;
 cudaError_t launch_laplace8(const void* a, void* out, int64_t B, cudaStream_t s) {
   auto k = batch_bulk_kernel<double, 8, 8, kLapTPB, kLapStages, Laplace8Op>;
   constexpr int kMats = kLapTPB / Laplace8Op::kLanes;

@@ -108,10 +108,13 @@ int main() {
       scale[i] = p * 40320.0 / 16777216.0;  // ~ per(|A|)
     }
     printf("classic glynn 8x8: %.4f ms  %.0f GB/s\n", ms, B * 520.0 / (ms * 1e-3) / 1e9);
-    run_bulk<8, 8, 64, 3, Laplace8OpT<4>>("lap8 w4", a, out, B, nsm, 4, ref, scale);
-    run_bulk<8, 8, 64, 3, Laplace8OpT<4>, true>("CO w4", a, out, B, nsm, 4, ref, scale);
-    run_bulk<8, 8, 64, 3, Laplace8OpT<2>>("lap8 w2", a, out, B, nsm, 4, ref, scale);
-    run_bulk<8, 8, 64, 3, Laplace8OpT<6>>("lap8 w6", a, out, B, nsm, 4, ref, scale);
+    run_bulk<8, 8, 32, 2, Laplace8TOp<32, 10>>("lap8T 32", a, out, B, nsm, 4, ref, scale);
+    run_bulk<8, 8, 32, 1, Laplace8TOp<32, 10>>("lap8T s1", a, out, B, nsm, 6, ref, scale);
+    run_bulk<8, 8, 32, 1, Laplace8TOp<32, 10>>("lap8T s1", a, out, B, nsm, 7, ref, scale);
+    run_bulk<8, 8, 32, 2, Laplace8TOp<32, 7>>("lap8T g7", a, out, B, nsm, 4, ref, scale);
+    run_bulk<8, 8, 32, 2, Laplace8TOp<32, 16>>("lap8T g16", a, out, B, nsm, 4, ref, scale);
+    run_bulk<8, 8, 32, 2, Laplace8TOp<32, 10>, true>("CO T32", a, out, B, nsm, 4, ref, scale);
+    run_bulk<8, 8, 32, 1, Laplace8TOp<32, 10>, true>("CO T32s1", a, out, B, nsm, 6, ref, scale);
     {
       const int64_t b2 = 150000;
       float ms2 = timeit([&] { batch_glynn_kernel<double, 8><<<(b2 + kBatchThreads - 1) / kBatchThreads, kBatchThreads, smem>>>(a, out, b2); }, 10);
