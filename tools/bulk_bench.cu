@@ -10,6 +10,17 @@
 #include "../paper_2510_03421_b200/csrc/batch_bulk.cuh"
 using namespace permb200;
 
+// streaming ceiling of the bulk pipeline: no arithmetic, one store per matrix
+struct NullOp {
+  static constexpr int kLanes = 1;
+  template <class R>
+  __device__ static void run(const double* tile, int64_t first, int cnt, double* out, int me, R&& release) {
+    const double x = tile[me * 40];
+    release();
+    if (me < cnt) out[first + me] = x;
+  }
+};
+
 template <typename K>
 float timeit(K launch, int reps) {
   launch();
@@ -148,6 +159,13 @@ int main() {
     }
     printf("classic combdp 4x10: %.4f ms  %.0f GB/s\n", ms, B * 328.0 / (ms * 1e-3) / 1e9);
     run_bulk<4, 10, 128, 2, PartitionOp<double, 4, 10>>("part4x10", a, out, B, nsm, 2, ref, scale);
+    run_bulk<4, 10, 128, 2, NullOp>("null", a, out, B, nsm, 2, ref, scale);
+    run_bulk<4, 10, 128, 3, NullOp>("null", a, out, B, nsm, 2, ref, scale);
+    run_bulk<4, 10, 256, 2, NullOp>("null", a, out, B, nsm, 1, ref, scale);
+    run_bulk<4, 10, 64, 4, NullOp>("null", a, out, B, nsm, 3, ref, scale);
+    run_bulk<4, 10, 128, 4, PartitionOp<double, 4, 10>>("part s4", a, out, B, nsm, 1, ref, scale);
+    run_bulk<4, 10, 64, 4, PartitionOp<double, 4, 10>>("part 64s4", a, out, B, nsm, 3, ref, scale);
+    run_bulk<4, 10, 64, 3, PartitionOp<double, 4, 10>>("part 64s3", a, out, B, nsm, 4, ref, scale);
     // streaming floor: a plain device copy of the same bytes
     double* c2;
     cudaMalloc(&c2, h.size() * 8);
