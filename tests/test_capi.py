@@ -115,3 +115,24 @@ def test_no_cpu_fallback_without_gpu():
 
     with pytest.raises(_lib.EngineUnavailable):
         P.glynn(np.random.default_rng(0).uniform(-1, 1, (5, 5)))
+
+
+def test_batch_shape_contracts_without_gpu():
+    """Shape validation of the batch entry points happens before any device
+    work, so it is exercised here: the partition formula stops at m = 6, the
+    Laplace formula is 8x8 only, non-Glynn batches stop at n = 16, square
+    Glynn batches at n = 30."""
+    import numpy as np
+
+    import paper_2510_03421_b200 as P
+
+    with pytest.raises(ValueError):
+        P.partition_batch(np.zeros((2, 7, 9)))
+    with pytest.raises(ValueError):
+        P.laplace_batch(np.zeros((2, 6, 6)))
+    with pytest.raises(ValueError):
+        P.ryser_batch(np.zeros((2, 17, 17)))
+    with pytest.raises(ValueError):
+        P.glynn_batch(np.zeros((2, 31, 31)))
+    with pytest.raises(ValueError):
+        P.opt_batch(np.zeros((2, 5, 20)))  # rectangular beyond n = 16
