@@ -369,6 +369,37 @@ struct PartitionOp {
   }
 };
 
+// Wide rectangles (16 < n <= 62, m <= 6): the same partition formula with a
+// runtime column count, one thread per matrix reading its rows straight from
+// global memory (sequential 8-byte loads through L1: every 32-byte sector a
+// thread touches is consumed by its next loads).
+template <typename T, int M>
+__global__ void __launch_bounds__(128) partition_rt_kernel(const T* __restrict__ a, T* __restrict__ out, int64_t nb,
+                                                           int n) {
+  using X = Num<T>;
+  constexpr int NS = 1 << M;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  const T* A = a + i * M * n;
+  T S[NS];
+#pragma unroll
+  for (int b = 0; b < NS; ++b) S[b] = X::zero();
+  for (int j = 0; j < n; ++j) {
+    T p[NS];
+#pragma unroll
+    for (int r = 0; r < M; ++r) p[1 << r] = A[r * n + j];
+#pragma unroll
+    for (int b = 3; b < NS; ++b) {
+      if ((b & (b - 1)) == 0) continue;
+      const int h = bb_hibit(b);
+      p[b] = X::mul(p[b ^ (1 << h)], p[1 << h]);
+    }
+#pragma unroll
+    for (int b = 1; b < NS; ++b) S[b] = X::add(S[b], p[b]);
+  }
+  out[i] = partition_combine<T, M>(S);
+}
+
 // ---------------------------------------------------- square 8x8: Laplace
 __host__ __device__ constexpr int lp_pidx(int i, int k) { return i * (15 - i) / 2 + (k - i - 1); }  // i < k < 8
 struct LpSub {

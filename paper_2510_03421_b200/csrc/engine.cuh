@@ -80,6 +80,8 @@ uint64_t walk_steps(int alg, int m, int n);
 bool bulk_batch_supported(int alg, bool cplx, int m, int n);
 // PERM_OK / CUDA failure, or -1 when no bulk kernel applies (shape, alignment)
 int launch_bulk_batch(int alg, bool cplx, int64_t B, int m, int n, const void* dA, void* dOut, cudaStream_t stream);
+// partition formula for 16 < n <= 62 (runtime n)
+int launch_partition_wide(bool cplx, int64_t B, int m, int n, const void* dA, void* dOut, cudaStream_t stream);
 
 // ---- instrumentation -------------------------------------------------------
 struct KernelTimer {

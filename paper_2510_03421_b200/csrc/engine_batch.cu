@@ -168,6 +168,7 @@ static int launch_walk_multi_batch(bool cplx, int64_t B, int n, const void* dA, 
 static int launch_batch(int alg, bool cplx, int64_t B, int m, int n, const void* dA, void* dOut,
                         cudaStream_t stream) {
   if (alg == PERM_ALG_GLYNN && m == n && n >= kWalkMultiMinN) return launch_walk_multi_batch(cplx, B, n, dA, dOut, stream);
+  if (alg == PERM_ALG_BATCH_PARTITION && n > 16) return launch_partition_wide(cplx, B, m, n, dA, dOut, stream);
   if (alg == PERM_ALG_BATCH_LAPLACE || alg == PERM_ALG_BATCH_PARTITION) {
     const int st = launch_bulk_batch(alg, cplx, B, m, n, dA, dOut, stream);
     if (st >= 0) return st;
@@ -317,7 +318,7 @@ int batch_select(int m, int n) {
   if (m == 8 && n == 8) return PERM_ALG_BATCH_LAPLACE;
   if (m == n) return PERM_ALG_GLYNN;
   if (m <= 4 || (m <= 6 && n >= m + 2)) return PERM_ALG_BATCH_PARTITION;
-  return PERM_ALG_RYSER;
+  return PERM_ALG_RYSER;  // (n <= 16 only: wider rectangles with m >= 7 are refused)
 }
 
 // ---------------------------------------------------------------------------
@@ -449,8 +450,10 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
     return PERM_BAD_SHAPE;
   }
   if (alg < 0) alg = batch_select(m, n);
-  if (n > 16 && !(m == n && alg == PERM_ALG_GLYNN && n <= kWalkMultiMaxN)) {
-    set_error("batched kernels handle n <= 16 (square Glynn: n <= 30); use the single-permanent entry points");
+  if (n > 16 && !(m == n && alg == PERM_ALG_GLYNN && n <= kWalkMultiMaxN) &&
+      !(alg == PERM_ALG_BATCH_PARTITION && n <= 62 && m <= (cplx ? 4 : 6))) {
+    set_error("batched kernels handle n <= 16 (square Glynn: n <= 30; the partition formula, m <= 6: n <= 62); "
+              "use the single-permanent entry points");
     return PERM_BAD_SHAPE;
   }
   if (alg > PERM_ALG_BATCH_LAPLACE) {

@@ -98,7 +98,34 @@ bulk_fn pick_partition(int m, int n, std::integer_sequence<int, Is...>) {
   return f;
 }
 
+template <typename T, int M>
+cudaError_t launch_partition_rt(const void* a, void* out, int64_t B, int n, cudaStream_t s) {
+  const int64_t grid = (B + 127) / 128;
+  partition_rt_kernel<T, M><<<(unsigned)grid, 128, 0, s>>>(static_cast<const T*>(a), static_cast<T*>(out), B, n);
+  return cudaGetLastError();
+}
+using rt_fn = cudaError_t (*)(const void*, void*, int64_t, int, cudaStream_t);
+template <typename T, int... Ms>
+rt_fn pick_rt(int m, std::integer_sequence<int, Ms...>) {
+  rt_fn f = nullptr;
+  ((m == Ms + 1 ? (f = &launch_partition_rt<T, Ms + 1>, 0) : 0), ...);
+  return f;
+}
+
 }  // namespace
+
+// Partition formula for wide rectangles, 16 < n <= 62 (m <= 6 real, m <= 4
+// complex): runtime-n kernel (no bulk staging).
+int launch_partition_wide(bool cplx, int64_t B, int m, int n, const void* dA, void* dOut, cudaStream_t stream) {
+  rt_fn fn = cplx ? pick_rt<cd>(m, std::make_integer_sequence<int, 4>{})
+                  : pick_rt<double>(m, std::make_integer_sequence<int, 6>{});
+  if (!fn || n > 62 || m > n) {
+    set_error("the partition batch formula covers m <= 6 (complex m <= 4), n <= 62");
+    return PERM_BAD_SHAPE;
+  }
+  const cudaError_t e = fn(dA, dOut, B, n, stream);
+  return e == cudaSuccess ? PERM_OK : cuda_fail(e, "partition batch launch");
+}
 
 bool bulk_batch_supported(int alg, bool cplx, int m, int n) {
   if (alg == PERM_ALG_BATCH_LAPLACE) return !cplx && m == 8 && n == 8;

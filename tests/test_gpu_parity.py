@@ -424,6 +424,34 @@ def test_batched_medium_walks(cplx):
         P.ryser_batch(rng.uniform(-1, 1, (2, 17, 17)))  # other algorithms stop at n = 16
 
 
+@pytest.mark.parametrize("cplx", [False, True])
+def test_partition_wide_rectangles(cplx):
+    """Partition formula for 16 < n <= 62 (runtime-n kernel): exact on
+    {-1, 0, 1} matrices (every intermediate is an integer below 2^53) against
+    the oracle's exact int64 Ryser-rect, and within metric (ii) on float
+    inputs against the oracle's combinatoric where that is affordable."""
+    rng = np.random.default_rng(4242 + cplx)
+    shapes = [(1, 40), (2, 62), (3, 20), (4, 33)] + ([] if cplx else [(5, 24), (6, 62)])
+    for m, n in shapes:
+        B = 37
+        Ai = rng.integers(-1, 2, (B, m, n))
+        A = Ai.astype(np.complex128 if cplx else np.float64)
+        out = P.partition_batch(A)
+        assert np.array_equal(out, P.opt_batch(A))
+        for i in (0, B - 1):
+            exact = O.permanent("ryser", Ai[i].astype(np.int64))
+            assert not exact[1] and out[i] == exact[0], (m, n, i)
+        if math.perm(n, m) <= 3_000_000:
+            F = rng.standard_normal((B, m, n)) / np.sqrt(n)
+            if cplx:
+                F = F + 1j * rng.standard_normal((B, m, n)) / np.sqrt(n)
+            fo = P.partition_batch(F)
+            mag = np.abs(P.partition_batch(np.abs(F)))
+            for i in (0, B - 1):
+                ref = O.permanent("combinatoric", F[i])[0]
+                assert abs(fo[i] - ref) <= TOL * max(abs(ref), mag[i]), (m, n, i)
+
+
 def _dd_value(a, alg):
     from paper_2510_03421_b200 import engine as E
 
