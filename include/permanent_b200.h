@@ -131,10 +131,10 @@ int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int
  * with n >= m + 2, subset-skipping Ryser otherwise).  PARTITION / LAPLACE stream the batch through shared
  * memory with 1-D bulk copies (persistent grid); other algorithms run one
  * thread (or warp) per matrix.
- * Requires m <= n <= 16, except square Glynn (alg GLYNN or the dispatch on a
- * square) up to n = 30 -- every matrix's Gray walk split into segments over
- * one launch (walk_multi_kernel), combined per matrix in segment order --
- * and PARTITION up to n = 62 (m <= 6, complex m <= 4).
+ * Requires m <= n <= 16, except Glynn up to n = 30 (square, or rectangular
+ * on the ones-padded 2^s-scaled matrix) -- every matrix's Gray walk split
+ * into segments over one launch (walk_multi_kernel), combined per matrix in
+ * segment order -- and PARTITION up to n = 62 (m <= 6, complex m <= 4).
  * Device-pointer calls are asynchronous on `stream`. */
 int perm_batch_f64(int alg, int64_t B, int m, int n, const double* a, double* out, int dev_ptr, void* stream);
 int perm_batch_c128(int alg, int64_t B, int m, int n, const double* a, double* out, int dev_ptr, void* stream);

@@ -135,10 +135,12 @@ static batch_fn pick_glynn_warp(int n, std::integer_sequence<int, Ns...>) {
 // the classic kernel of the same family: Laplace -> Glynn, partition ->
 // memoized combinatoric).  Thread-per-matrix needs enough matrices to fill
 // the GPU; below that a warp per matrix (n >= 9).
-// Square Glynn batches of n = 17..30: every matrix's Gray walk split into
+// Glynn batches of n = 17..30 (square, or rectangular on the ones-padded,
+// 2^s-scaled matrix): every matrix's Gray walk split into
 // segments over the grid (walk_multi_kernel), partials combined per matrix
 // in segment order inside the launch.
-static int launch_walk_multi_batch(bool cplx, int64_t B, int n, const void* dA, void* dOut, cudaStream_t stream) {
+static int launch_walk_multi_batch(bool cplx, int64_t B, int m, int n, const void* dA, void* dOut,
+                                   cudaStream_t stream) {
   walk_multi_fn fn = walk_multi_lookup(cplx, n);
   walk_multi_bps_fn bfn = walk_multi_bps_lookup(cplx, n);
   if (!fn || !bfn) {
@@ -159,7 +161,7 @@ static int launch_walk_multi_batch(bool cplx, int64_t B, int n, const void* dA, 
   unsigned int* done = static_cast<unsigned int*>(scratch);
   double* partials = reinterpret_cast<double*>(static_cast<char*>(scratch) + done_bytes);
   cudaError_t e = cudaMemsetAsync(done, 0, (size_t)B * sizeof(unsigned int), stream);
-  if (e == cudaSuccess) e = fn(dA, dOut, B, partials, done, pl, stream);
+  if (e == cudaSuccess) e = fn(dA, dOut, B, m, partials, done, pl, stream);
   const cudaError_t ef = cudaFreeAsync(scratch, stream);
   if (e == cudaSuccess) e = ef;
   return e == cudaSuccess ? PERM_OK : cuda_fail(e, "batched walk launch");
@@ -167,7 +169,7 @@ static int launch_walk_multi_batch(bool cplx, int64_t B, int n, const void* dA, 
 
 static int launch_batch(int alg, bool cplx, int64_t B, int m, int n, const void* dA, void* dOut,
                         cudaStream_t stream) {
-  if (alg == PERM_ALG_GLYNN && m == n && n >= kWalkMultiMinN) return launch_walk_multi_batch(cplx, B, n, dA, dOut, stream);
+  if (alg == PERM_ALG_GLYNN && n >= kWalkMultiMinN) return launch_walk_multi_batch(cplx, B, m, n, dA, dOut, stream);
   if (alg == PERM_ALG_BATCH_PARTITION && n > 16) return launch_partition_wide(cplx, B, m, n, dA, dOut, stream);
   if (alg == PERM_ALG_BATCH_LAPLACE || alg == PERM_ALG_BATCH_PARTITION) {
     const int st = launch_bulk_batch(alg, cplx, B, m, n, dA, dOut, stream);
@@ -318,7 +320,8 @@ int batch_select(int m, int n) {
   if (m == 8 && n == 8) return PERM_ALG_BATCH_LAPLACE;
   if (m == n) return PERM_ALG_GLYNN;
   if (m <= 4 || (m <= 6 && n >= m + 2)) return PERM_ALG_BATCH_PARTITION;
-  return PERM_ALG_RYSER;  // (n <= 16 only: wider rectangles with m >= 7 are refused)
+  if (n > 16) return PERM_ALG_GLYNN;  // batched walks (pre-scaled, ones-padded) up to n = 30
+  return PERM_ALG_RYSER;
 }
 
 // ---------------------------------------------------------------------------
@@ -450,9 +453,9 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
     return PERM_BAD_SHAPE;
   }
   if (alg < 0) alg = batch_select(m, n);
-  if (n > 16 && !(m == n && alg == PERM_ALG_GLYNN && n <= kWalkMultiMaxN) &&
+  if (n > 16 && !(alg == PERM_ALG_GLYNN && n <= kWalkMultiMaxN) &&
       !(alg == PERM_ALG_BATCH_PARTITION && n <= 62 && m <= (cplx ? 4 : 6))) {
-    set_error("batched kernels handle n <= 16 (square Glynn: n <= 30; the partition formula, m <= 6: n <= 62); "
+    set_error("batched kernels handle n <= 16 (Glynn: n <= 30; the partition formula, m <= 6: n <= 62); "
               "use the single-permanent entry points");
     return PERM_BAD_SHAPE;
   }

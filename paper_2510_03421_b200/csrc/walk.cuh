@@ -635,14 +635,15 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_ke
 // writes a block partial, and the last segment of a matrix to finish
 // (per-matrix counter) combines its segments in order -> out[matrix].
 struct WalkMultiArgs {
-  const void* a;          // [nmats][P][P] row-major, device
+  const void* a;          // [nmats][m][P] row-major, device
   void* out;              // [nmats] permanents
   double* partials;       // [nmats * segs][kPartialStride]
   unsigned int* done;     // [nmats], zero on entry, reset on exit
   int64_t nmats;
+  int m;                  // rows (m < P: rectangular Glynn on [2^s A; J])
   int segs, log2L;
   uint64_t groups_per_seg;
-  double scale;           // 2^-(n-1)
+  double scale;           // 2^-(n-1) / (n-m)!
 };
 
 template <typename T, int P>
@@ -659,16 +660,55 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_mu
   for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
     const int64_t mat = w / args.segs;
     const int seg = (int)(w - mat * args.segs);
-    const T* A = static_cast<const T*>(args.a) + mat * P * P;
+    const int m = args.m;
+    const T* A = static_cast<const T*>(args.a) + mat * m * P;
     __syncthreads();  // previous item's shared memory is free
+    // rectangular: ones rows below the m real rows, which are pre-scaled by
+    // 2^s, s = round(-log2 RMS of the nonzero entries) (as prescale_log2)
+    int sl = 0;
+    if (m < P) {
+      double ss = 0.0;
+      int nz = 0;
+      for (int i = tid; i < m * P; i += kWalkThreads) {
+        const double q = Num<T>::re(A[i]) * Num<T>::re(A[i]) + Num<T>::im(A[i]) * Num<T>::im(A[i]);
+        if (q != 0.0) {
+          ss += q;
+          ++nz;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        ss += __shfl_down_sync(0xffffffffu, ss, off);
+        nz += __shfl_down_sync(0xffffffffu, nz, off);
+      }
+      __shared__ double red_ss[kWalkWarps];
+      __shared__ int red_nz[kWalkWarps];
+      if ((tid & 31) == 0) {
+        red_ss[warp] = ss;
+        red_nz[warp] = nz;
+      }
+      __syncthreads();
+      double S = 0.0;
+      int Z = 0;
+      for (int w2 = 0; w2 < kWalkWarps; ++w2) {
+        S += red_ss[w2];
+        Z += red_nz[w2];
+      }
+      if (Z > 0 && S > 0.0) {
+        const double e = -0.5 * log2(S / Z);
+        if (isfinite(e)) sl = (int)rint(e);
+      }
+    }
+    const double k = ldexp(1.0, sl);
     for (int i = tid; i < B * P; i += kWalkThreads) {
       const int t = i / P, j = i - t * P;
-      sU[t * PS + j] = Num<T>::scale(-2.0, A[(P - 1 - t) * P + j]);
+      const int row = P - 1 - t;
+      sU[t * PS + j] = (row < m) ? Num<T>::scale(-2.0 * k, A[row * P + j]) : Num<T>::scale(-2.0, Num<T>::one());
     }
     for (int j = tid; j < P; j += kWalkThreads) {
-      T c = A[j];
-      for (int i = 1; i < P; ++i) c = Num<T>::add(c, A[i * P + j]);
-      sV0[j] = c;
+      T c = Num<T>::zero();
+      for (int i = 0; i < m; ++i) c = Num<T>::add(c, A[i * P + j]);
+      sV0[j] = Num<T>::add(Num<T>::scale(k, c), Num<T>::scale((double)(P - m), Num<T>::one()));
     }
     __syncthreads();
     WalkRow0<T, P> u0;
@@ -695,9 +735,10 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_mu
         dd_add(H, Lo, p[s * kPartialStride], p[s * kPartialStride + 1]);
         dd_add(H2, L2, p[s * kPartialStride + 2], p[s * kPartialStride + 3]);
       }
+      const double sc = args.scale * ldexp(1.0, -sl * m);
       T r;
-      if constexpr (sizeof(T) == 16) r = cd_make((H + Lo) * args.scale, (H2 + L2) * args.scale);
-      else r = (H + Lo) * args.scale;
+      if constexpr (sizeof(T) == 16) r = cd_make((H + Lo) * sc, (H2 + L2) * sc);
+      else r = (H + Lo) * sc;
       static_cast<T*>(args.out)[mat] = r;
       args.done[mat] = 0u;
     }

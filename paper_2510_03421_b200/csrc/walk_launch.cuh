@@ -175,7 +175,7 @@ inline WalkMultiPlan plan_walk_multi(int n, int64_t nmats, int nsm, int bps) {
 }
 
 template <typename T, int P>
-cudaError_t launch_walk_multi(const void* a, void* out, int64_t nmats, double* partials, unsigned int* done,
+cudaError_t launch_walk_multi(const void* a, void* out, int64_t nmats, int m, double* partials, unsigned int* done,
                               const WalkMultiPlan& pl, cudaStream_t stream) {
   constexpr int PS = row_stride<T, P>();
   const size_t smem = (size_t)((P - 1) * PS + PS + kWalkWarps * PS) * sizeof(T);
@@ -185,10 +185,13 @@ cudaError_t launch_walk_multi(const void* a, void* out, int64_t nmats, double* p
   args.partials = partials;
   args.done = done;
   args.nmats = nmats;
+  args.m = m;
   args.segs = pl.segs;
   args.log2L = pl.log2L;
   args.groups_per_seg = pl.groups_per_seg;
-  args.scale = std::ldexp(1.0, -(P - 1));
+  double f = 1.0;
+  for (int i = 2; i <= P - m; ++i) f *= (double)i;
+  args.scale = std::ldexp(1.0, -(P - 1)) / f;
   walk_multi_kernel<T, P><<<pl.grid, kWalkThreads, smem, stream>>>(args);
   return cudaGetLastError();
 }
@@ -201,8 +204,8 @@ int walk_multi_blocks_per_sm() {
     bps = 1;
   return bps < 1 ? 1 : bps;
 }
-using walk_multi_fn = cudaError_t (*)(const void*, void*, int64_t, double*, unsigned int*, const WalkMultiPlan&,
-                                      cudaStream_t);
+using walk_multi_fn = cudaError_t (*)(const void*, void*, int64_t, int, double*, unsigned int*,
+                                      const WalkMultiPlan&, cudaStream_t);
 using walk_multi_bps_fn = int (*)();
 // walk_multi_inst.cu: P = 17..30, double and cd
 walk_multi_fn walk_multi_lookup(bool cplx, int P);

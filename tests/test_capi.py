@@ -121,7 +121,7 @@ def test_batch_shape_contracts_without_gpu():
     """Shape validation of the batch entry points happens before any device
     work, so it is exercised here: the partition formula stops at m = 6 and
     n = 62 (complex beyond n = 16: m <= 4), the Laplace formula is 8x8 only,
-    other batches stop at n = 16, square Glynn batches at n = 30."""
+    Glynn batches stop at n = 30, the other algorithms at n = 16."""
     import numpy as np
 
     import paper_2510_03421_b200 as P
@@ -135,7 +135,7 @@ def test_batch_shape_contracts_without_gpu():
     with pytest.raises(ValueError):
         P.glynn_batch(np.zeros((2, 31, 31)))
     with pytest.raises(ValueError):
-        P.opt_batch(np.zeros((2, 7, 20)))  # m >= 7 rectangles stop at n = 16
+        P.opt_batch(np.zeros((2, 7, 31)))  # m >= 7 rectangles: batched walks stop at n = 30
     with pytest.raises(ValueError):
         P.partition_batch(np.zeros((2, 5, 63)))  # 62 columns at most
     with pytest.raises(ValueError):

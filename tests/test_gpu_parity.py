@@ -400,7 +400,8 @@ def test_laplace_batch_8x8():
 
 @pytest.mark.parametrize("cplx", [False, True])
 def test_batched_medium_walks(cplx):
-    """Square Glynn batches of n = 17..30 (one launch, segments per matrix):
+    """Glynn batches of n = 17..30 (one launch, segments per matrix), square
+    and rectangular:
     every result equals the single-matrix engine's within metric (ii), and
     matches the oracle's double-double walk for n <= 20; batch sizes from 1
     (many segments per matrix) to a few hundred (one segment each)."""
@@ -420,6 +421,20 @@ def test_batched_medium_walks(cplx):
             if n <= 20:
                 ref = O.dd_permanent("glynn", A[i], nthreads=8)
                 assert scaled_err(out[i], ref, M) <= TOL, (n, B, i)
+    # rectangular (ones-padded, pre-scaled per matrix inside the kernel)
+    for m, n, B in ((7, 17, 9), (12, 20, 5), (18, 22, 3), (25, 28, 2)):
+        A = rng.uniform(-1, 1, (B, m, n)) / n
+        if cplx:
+            A = A + 1j * rng.uniform(-1, 1, (B, m, n)) / n
+        out = P.glynn_batch(A)
+        if m >= 7:
+            assert np.array_equal(out, P.opt_batch(A))  # the batch dispatch's choice for m >= 7, n > 16
+        for i in sorted({0, B - 1}):
+            v, M = P.permanent_with_magsum(as_matrix(A[i]), AlgorithmId.GLYNN)
+            assert scaled_err(out[i], v, M) <= TOL, (m, n, i)
+            if n <= 20:
+                ref = O.dd_permanent("glynn", A[i], nthreads=8)
+                assert scaled_err(out[i], ref, M) <= TOL, (m, n, i)
     with pytest.raises(ValueError):
         P.ryser_batch(rng.uniform(-1, 1, (2, 17, 17)))  # other algorithms stop at n = 16
 
