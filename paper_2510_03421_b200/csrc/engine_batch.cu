@@ -414,6 +414,7 @@ int tiny_permanent(int alg, bool cplx, int m, int n, const double* a, double* ou
   // square kernel runs; per(A) = per([2^s A; J]) / ((n-m)! 2^(s m)).
   const bool pad = (alg == PERM_ALG_GLYNN && m < n && n <= 12);
   double unscale = 1.0;
+  int unscale_exp = 0;
   if (pad) {
     if ((size_t)n * n * esz > TinyBuf::kIn) return -1;
     HostMat A;
@@ -431,7 +432,8 @@ int tiny_permanent(int alg, bool cplx, int m, int n, const double* a, double* ou
           h[((size_t)i * n + j) * w + c] = (i < m) ? a[((size_t)i * n + j) * w + c] * k : (c == 0 ? 1.0 : 0.0);
     double f = 1.0;
     for (int i = 2; i <= n - m; ++i) f *= (double)i;
-    unscale = std::ldexp(1.0, -sl * m) / f;
+    unscale = 1.0 / f;
+    unscale_exp = -sl * m;  // applied with ldexp on the value (the factor alone can underflow)
   } else {
     std::memcpy(tb.host, a, bytes);
   }
@@ -439,8 +441,8 @@ int tiny_permanent(int alg, bool cplx, int m, int n, const double* a, double* ou
   if (st != PERM_OK) return st;
   std::memcpy(out, tb.host + TinyBuf::kIn, esz);
   if (pad) {
-    out[0] *= unscale;
-    if (cplx) out[1] *= unscale;
+    out[0] = std::ldexp(out[0] * unscale, unscale_exp);
+    if (cplx) out[1] = std::ldexp(out[1] * unscale, unscale_exp);
   }
   return PERM_OK;
 }

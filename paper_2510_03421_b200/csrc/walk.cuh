@@ -735,10 +735,12 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_mu
         dd_add(H, Lo, p[s * kPartialStride], p[s * kPartialStride + 1]);
         dd_add(H2, L2, p[s * kPartialStride + 2], p[s * kPartialStride + 3]);
       }
-      const double sc = args.scale * ldexp(1.0, -sl * m);
+      // 2^(-s m) applied with ldexp on the value (the factor alone can
+      // underflow where the permanent does not)
       T r;
-      if constexpr (sizeof(T) == 16) r = cd_make((H + Lo) * sc, (H2 + L2) * sc);
-      else r = (H + Lo) * sc;
+      if constexpr (sizeof(T) == 16)
+        r = cd_make(ldexp((H + Lo) * args.scale, -sl * m), ldexp((H2 + L2) * args.scale, -sl * m));
+      else r = ldexp((H + Lo) * args.scale, -sl * m);
       static_cast<T*>(args.out)[mat] = r;
       args.done[mat] = 0u;
     }

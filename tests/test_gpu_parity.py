@@ -435,6 +435,17 @@ def test_batched_medium_walks(cplx):
             if n <= 20:
                 ref = O.dd_permanent("glynn", A[i], nthreads=8)
                 assert scaled_err(out[i], ref, M) <= TOL, (m, n, i)
+    # powers of two commute with every operation of the walk (no rounding
+    # changes), and the per-matrix pre-scale of rectangles follows them
+    # exactly: scaling the entries by 2^-40 scales every result by exactly
+    # 2^(-40 m), square or rectangular
+    for m, n in ((12, 20), (20, 20)):
+        A = rng.uniform(-1, 1, (3, m, n)) / n
+        if cplx:
+            A = A + 1j * rng.uniform(-1, 1, (3, m, n)) / n
+        base = P.glynn_batch(A)
+        scaled = P.glynn_batch(A * 2.0 ** -40)
+        assert np.array_equal(scaled, base * 2.0 ** (-40 * m)), (m, n)
     with pytest.raises(ValueError):
         P.ryser_batch(rng.uniform(-1, 1, (2, 17, 17)))  # other algorithms stop at n = 16
 
