@@ -135,6 +135,11 @@ static batch_fn pick_glynn_warp(int n, std::integer_sequence<int, Ns...>) {
 // the classic kernel of the same family: Laplace -> Glynn, partition ->
 // memoized combinatoric).  Thread-per-matrix needs enough matrices to fill
 // the GPU; below that a warp per matrix (n >= 9).
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
 // Glynn batches of n = 17..30 (square, or rectangular on the ones-padded,
 // 2^s-scaled matrix): every matrix's Gray walk split into
 // segments over the grid (walk_multi_kernel), partials combined per matrix
@@ -182,7 +187,10 @@ static int launch_batch(int alg, bool cplx, int64_t B, int m, int n, const void*
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   batch_fn fn = nullptr;
-  if (alg == PERM_ALG_GLYNN && m == n && n >= 9 && n <= 16 && B < (int64_t)nsm * 512)
+  // large batches: warp per matrix from n = 12 (n = 9..11 thread per matrix is faster; n = 13..16 has no
+  // thread-per-matrix template; measured with tools/batch_glynn_large.py)
+  static const int warp_min_n = env_int("PERM_BATCH_WARP_MIN_N", 12);
+  if (alg == PERM_ALG_GLYNN && m == n && n >= 9 && n <= 16 && (B < (int64_t)nsm * 512 || n >= warp_min_n))
     fn = cplx ? pick_glynn_warp<cd>(n, std::make_integer_sequence<int, 8>{})
               : pick_glynn_warp<double>(n, std::make_integer_sequence<int, 8>{});
   if (!fn && alg == PERM_ALG_GLYNN && m == n && n >= 2 && n <= 12)
@@ -296,10 +304,6 @@ class CopyPool {
   size_t bytes_ = 0;
 };
 
-static int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::atoi(v) : dflt;
-}
 
 static void par_memcpy(void* dst, const void* src, size_t bytes) {
   static CopyPool* pool = new CopyPool();  // detached workers: never destroyed
