@@ -128,7 +128,8 @@ int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int
  * out = [B] (same memory space).  alg = PERM_ALG_* (incl. the batch-only
  * formulas) or -1 for the batch dispatch (perm_batch_select: LAPLACE for 8x8
  * real, Glynn for other squares, PARTITION for m <= 4 < n and for m = 5, 6
- * with n >= m + 2, subset-skipping Ryser otherwise).  PARTITION / LAPLACE stream the batch through shared
+ * with n >= m + 2, Glynn on the ones-padded pre-scaled matrix for the other
+ * rectangles with n >= 9, subset-skipping Ryser otherwise).  PARTITION / LAPLACE stream the batch through shared
  * memory with 1-D bulk copies (persistent grid); other algorithms run one
  * thread (or warp) per matrix.
  * Requires m <= n <= 16, except Glynn up to n = 30 (square, or rectangular

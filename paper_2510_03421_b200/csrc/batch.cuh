@@ -173,7 +173,10 @@ constexpr int kBatchWarpMats = 8;  // matrices (warps) per block
 
 template <typename T, int N>
 __global__ void __launch_bounds__(32 * kBatchWarpMats) batch_glynn_warp_kernel(const T* __restrict__ a,
-                                                                              T* __restrict__ out, int64_t nbatch) {
+                                                                              T* __restrict__ out, int64_t nbatch,
+                                                                              int m) {
+  // m < N: rectangular Glynn on [2^s A; J] (ones rows below the m real rows,
+  // s = round(-log2 RMS of the nonzero entries) per matrix, as prescale_log2)
   constexpr int PS = row_stride<T, N>();
   constexpr int SLOT = (N - 1) * PS + PS;  // U rows + column sums
   __shared__ __align__(16) T smem[kBatchWarpMats * SLOT];
@@ -182,15 +185,38 @@ __global__ void __launch_bounds__(32 * kBatchWarpMats) batch_glynn_warp_kernel(c
   if (mat >= nbatch) return;  // whole warp exits together
   T* sU = smem + warp * SLOT;
   T* sV0 = sU + (N - 1) * PS;
-  const T* A = a + mat * N * N;
+  const T* A = a + mat * m * N;
+  int sl = 0;
+  if (m < N) {
+    double ss = 0.0;
+    int nz = 0;
+    for (int e = lane; e < m * N; e += 32) {
+      const double q = Num<T>::re(A[e]) * Num<T>::re(A[e]) + Num<T>::im(A[e]) * Num<T>::im(A[e]);
+      if (q != 0.0) {
+        ss += q;
+        ++nz;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      nz += __shfl_xor_sync(0xffffffffu, nz, off);
+    }
+    if (nz > 0 && ss > 0.0) {
+      const double e = -0.5 * log2(ss / nz);
+      if (isfinite(e)) sl = (int)rint(e);
+    }
+  }
+  const double k = ldexp(1.0, sl);
   for (int e = lane; e < N * N; e += 32) {
     const int i = e / N, j = e - i * N;
-    if (i >= 1) sU[(N - 1 - i) * PS + j] = Num<T>::scale(-2.0, A[e]);  // U[t] = -2 row(N-1-t)
+    if (i >= 1)  // U[t] = -2 row(N-1-t)
+      sU[(N - 1 - i) * PS + j] = (i < m) ? Num<T>::scale(-2.0 * k, A[e]) : Num<T>::scale(-2.0, Num<T>::one());
   }
   for (int j = lane; j < N; j += 32) {
-    T s = A[j];
-    for (int i = 1; i < N; ++i) s = Num<T>::add(s, A[i * N + j]);
-    sV0[j] = s;
+    T s = Num<T>::zero();
+    for (int i = 0; i < m; ++i) s = Num<T>::add(s, A[i * N + j]);
+    sV0[j] = Num<T>::add(Num<T>::scale(k, s), Num<T>::scale((double)(N - m), Num<T>::one()));
   }
   __syncwarp();
   constexpr int LOG2L = N - 1 - 5;
@@ -212,7 +238,13 @@ __global__ void __launch_bounds__(32 * kBatchWarpMats) batch_glynn_warp_kernel(c
       acc.y += __shfl_down_sync(0xffffffffu, acc.y, off);
     }
   }
-  if (lane == 0) out[mat] = Num<T>::scale(1.0 / (double)(1 << (N - 1)), acc);
+  if (lane == 0) {
+    double f = (double)(1 << (N - 1));
+    for (int i = 2; i <= N - m; ++i) f *= (double)i;
+    const T r = Num<T>::scale(1.0 / f, acc);
+    if constexpr (sizeof(T) == 8) out[mat] = ldexp(r, -sl * m);
+    else out[mat] = cd_make(ldexp(r.x, -sl * m), ldexp(r.y, -sl * m));
+  }
 }
 
 // ---------------------------------------------------------------- Ryser

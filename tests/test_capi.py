@@ -57,7 +57,7 @@ def test_version_and_select():
 def test_batch_select():
     """Batch dispatch: the 4+4 Laplace formula for 8x8 (4), the partition
     formula (3) for m <= 4 < n and m = 5, 6 with n >= m + 2, Glynn for other
-    squares, Ryser otherwise."""
+    squares and for the remaining rectangles with n >= 9, Ryser otherwise."""
     lib = _lib.load()
     assert lib.perm_batch_select(8, 8) == 4
     assert lib.perm_batch_select(4, 10) == 3
@@ -67,7 +67,9 @@ def test_batch_select():
     assert lib.perm_batch_select(5, 6) == _lib.ALG_RYSER
     assert lib.perm_batch_select(6, 8) == 3
     assert lib.perm_batch_select(6, 7) == _lib.ALG_RYSER
-    assert lib.perm_batch_select(7, 12) == _lib.ALG_RYSER
+    assert lib.perm_batch_select(7, 8) == _lib.ALG_RYSER
+    assert lib.perm_batch_select(7, 12) == _lib.ALG_GLYNN
+    assert lib.perm_batch_select(12, 16) == _lib.ALG_GLYNN
 
 
 @pytest.mark.parametrize("alg,m,n", [(2, 36, 36), (2, 20, 28), (1, 30, 30), (1, 5, 33), (2, 3, 3)])
