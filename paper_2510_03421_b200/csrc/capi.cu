@@ -91,10 +91,11 @@ int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, 
     }
     return batch_permanent(alg, cplx, 1, m, n, a, out, 0, stream_);
   }
-  // square Glynn n = 9..TINY_GLYNN_MAX_N: one warp walks the matrix (the
+  // Glynn n = 9..TINY_GLYNN_MAX_N (rectangles ones-padded and pre-scaled on the
+  // host): one warp walks the matrix (the
   // warp-per-matrix batch kernel) on the zero-copy path, cheaper than a
   // device-wide walk launch at these sizes
-  if (magsum == nullptr && !dev_ptr && lda == n && stream_ == nullptr && alg == PERM_ALG_GLYNN && m == n &&
+  if (magsum == nullptr && !dev_ptr && lda == n && stream_ == nullptr && alg == PERM_ALG_GLYNN &&
       n <= tiny_glynn_max_n()) {
     const int tst = tiny_permanent(alg, cplx, m, n, a, out);
     if (tst >= 0) return tst;
