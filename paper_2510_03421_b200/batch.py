@@ -81,8 +81,10 @@ def _run(a, alg):
 def opt_batch(a, params=None):
     """Permanents of a [B, m, n] batch with the batch dispatch
     (perm_batch_select: Laplace for 8x8 real, Glynn for other squares, the
-    partition formula for m <= 4 < n and m = 5, 6 with n >= m + 2,
-    subset-skipping Ryser otherwise)."""
+    partition formula for m <= 4 < n and m = 5, 6 with n >= m + 2, Glynn on
+    the ones-padded pre-scaled matrix for the other rectangles with n >= 9,
+    subset-skipping Ryser otherwise).  Shapes: m <= n <= 30, and the
+    partition formula up to n = 62."""
     return _run(a, None)
 
 
