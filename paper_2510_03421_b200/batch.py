@@ -10,8 +10,9 @@ matrix than any of the reference's algorithms: the set-partition (Moebius)
 formula for m <= 6 and the 4+4 Laplace expansion for 8x8, both streamed
 through shared memory by bulk copies (csrc/batch_bulk.cuh).
 
-Float64 / complex128 batches only; integer batches are routed through the
-exact single-matrix path (one call each), keeping its semantics.
+Integer batches return exact Python ints with the single-matrix semantics:
+matrices whose magnitudes certify exact FP64 arithmetic run on the batch
+kernels, the rest through the exact single-matrix path (``_int_batch``).
 """
 from __future__ import annotations
 
@@ -58,10 +59,7 @@ def _run(a, alg):
     if arr.shape[1] > arr.shape[2]:
         arr = np.swapaxes(arr, 1, 2)
     if arr.dtype.kind in "iub":
-        from . import opt, glynn, ryser, combinatoric
-
-        fn = {-1: opt, 0: combinatoric, 1: ryser, 2: glynn}[code]
-        return np.array([fn(x) for x in arr], dtype=object)
+        return _int_batch(arr, code)
     cplx = np.iscomplexobj(arr)
     arr = np.ascontiguousarray(arr, dtype=np.complex128 if cplx else np.float64)
     B, m, n = arr.shape
@@ -75,6 +73,51 @@ def _run(a, alg):
 
         raise StepBudgetExceeded(_lib.last_error())
     _lib.check(st, f"batch {B}x{m}x{n}")
+    return out
+
+
+def _int_batch(arr, code):
+    """Integer batches: exact Python ints with the single-matrix semantics.
+
+    Matrices whose magnitudes certify that every intermediate of the batch
+    formula is an integer below 2^52 run on the float batch kernels, where
+    FP64 is then exact: the partition / Laplace formulas need
+    m! * prod_i (row sum of |a|) < 2^52 (every partial sum is a signed sum of
+    permanent monomials of |A|, weighted by at most m! in total), square
+    Glynn needs 2^(n-1) * prod_j (column sum of |a|) < 2^52.  Under the same
+    bounds none of the reference's checked int64 algorithms can overflow
+    either, so the result equals the per-matrix call.  Every other matrix
+    (and every explicit glynn / ryser / combinatoric request, which keeps its
+    own overflow semantics) goes through the exact single-matrix path."""
+    import math
+
+    from . import combinatoric, glynn, opt, ryser
+
+    per_matrix = {-1: opt, 0: combinatoric, 1: ryser, 2: glynn, 3: opt, 4: opt}[code]
+    B, m, n = arr.shape
+    out = np.empty(B, dtype=object)
+    if B == 0:
+        return out
+    certified = np.zeros(B, dtype=bool)
+    sel = int(_lib.load().perm_batch_select(m, n)) if code == -1 else code
+    if code in (-1, 3, 4) and (sel in (3, 4) or (sel == 2 and m == n)):
+        x = arr.astype(np.float64)
+        ax = np.abs(x)
+        with np.errstate(over="ignore", invalid="ignore"):
+            if sel in (3, 4):
+                bound = math.factorial(m) * np.prod(ax.sum(axis=2), axis=1)
+            else:
+                bound = 2.0 ** (n - 1) * np.prod(ax.sum(axis=1), axis=1)
+        certified = np.isfinite(bound) & (bound < 2.0 ** 52)
+        if certified.any():
+            sub = np.ascontiguousarray(x[certified])
+            vals = np.empty(sub.shape[0])
+            fn = _lib.load().perm_batch_f64
+            st = fn(sel, sub.shape[0], m, n, C.c_void_p(sub.ctypes.data), C.c_void_p(vals.ctypes.data), 0, None)
+            _lib.check(st, f"batch {sub.shape[0]}x{m}x{n}")
+            out[certified] = [int(v) for v in np.rint(vals)]
+    for i in np.nonzero(~certified)[0]:
+        out[i] = per_matrix(arr[i])
     return out
 
 

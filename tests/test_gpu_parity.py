@@ -636,3 +636,30 @@ def test_randomized_shapes_all_paths():
                 for i in (0, B - 1):
                     r = O.permanent(ref_alg, A[i])[0]
                     assert scaled_err(out[i], r, magsum(A[i])) <= TOL, (case, bfn.__name__, m, n, i)
+
+
+def test_integer_batches_exact():
+    """Integer batches: certified matrices run on the float batch kernels
+    (exact there), the rest per matrix; every value equals the oracle's exact
+    integer, and a matrix whose intermediates overflow int64 keeps the
+    reference's OverflowError semantics through opt."""
+    rng = np.random.default_rng(99)
+    cases = [(rng.random((300, 8, 8)) < 0.5).astype(np.int64),          # Laplace
+             rng.integers(-2, 3, (200, 4, 10)).astype(np.int64),         # partition
+             (rng.random((100, 12, 12)) < 0.5).astype(np.int64),        # Glynn, warp per matrix
+             rng.integers(-3, 4, (100, 5, 5)).astype(np.int64),          # Glynn, thread per matrix
+             (rng.random((50, 6, 20)) < 0.5).astype(np.int64)]          # partition, wide
+    for A in cases:
+        out = P.opt_batch(A)
+        m, n = A.shape[1:]
+        for i in (0, A.shape[0] // 2, A.shape[0] - 1):
+            ref = O.permanent("combinatoric" if math.perm(n, m) < 5e6 else ("glynn" if m == n else "ryser"), A[i])
+            assert not ref[1] and out[i] == ref[0], (A.shape, i)
+    # a mixed batch: the big-entry matrix is not certified and goes per matrix
+    M = np.stack([np.eye(8, dtype=np.int64), np.full((8, 8), 10, dtype=np.int64)])
+    out = P.opt_batch(M)
+    assert out[0] == 1
+    assert out[1] == 10 ** 8 * math.factorial(8) == P.opt(M[1])
+    with pytest.raises(OverflowError):  # as P.opt on that matrix
+        P.opt_batch(np.stack([np.eye(8, dtype=np.int64), np.full((8, 8), 1000, dtype=np.int64)]))
+    assert list(P.partition_batch(np.ones((3, 2, 5), dtype=np.int64))) == [20, 20, 20]
