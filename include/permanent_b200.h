@@ -43,7 +43,7 @@ enum {
 /* algorithm ids, same order as AlgorithmId in src/algorithms.py:26-31 */
 enum { PERM_ALG_COMBINATORIC = 0, PERM_ALG_RYSER = 1, PERM_ALG_GLYNN = 2 };
 /* batch-only formulas (perm_batch_*; no reference counterpart, exact algebra):
- * PARTITION = Moebius inversion over set partitions of the rows, m <= 6 (complex m <= 4);
+ * PARTITION = Moebius inversion over set partitions of the rows, m <= 6 (complex m <= 5);
  * LAPLACE = 4+4-row Laplace expansion from 2x2 row-pair permanents, 8x8 real. */
 enum { PERM_ALG_BATCH_PARTITION = 3, PERM_ALG_BATCH_LAPLACE = 4 };
 
@@ -135,7 +135,7 @@ int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int
  * Requires m <= n <= 16, except Glynn up to n = 30 (square, or rectangular
  * on the ones-padded 2^s-scaled matrix) -- every matrix's Gray walk split
  * into segments over one launch (walk_multi_kernel), combined per matrix in
- * segment order -- and PARTITION up to n = 62 (m <= 6, complex m <= 4).
+ * segment order -- and PARTITION up to n = 62 (m <= 6, complex m <= 5).
  * Device-pointer calls are asynchronous on `stream`. */
 int perm_batch_f64(int alg, int64_t B, int m, int n, const double* a, double* out, int dev_ptr, void* stream);
 int perm_batch_c128(int alg, int64_t B, int m, int n, const double* a, double* out, int dev_ptr, void* stream);

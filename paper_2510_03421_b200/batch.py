@@ -132,7 +132,7 @@ def opt_batch(a, params=None):
 
 
 def partition_batch(a):
-    """m <= 6 (complex m <= 4): sum over set partitions pi of the rows of
+    """m <= 6 (complex m <= 5): sum over set partitions pi of the rows of
     mu(pi) prod_{blocks b} sum_j prod_{i in b} a_ij."""
     return _run(a, "partition")
 

@@ -468,9 +468,13 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
     set_error(m > n ? "need m <= n; transpose first" : "bad batch shape");
     return PERM_BAD_SHAPE;
   }
-  if (alg < 0) alg = batch_select(m, n);
+  if (alg < 0) {
+    alg = batch_select(m, n);
+    // the complex partition formula stops at m = 5 (register file)
+    if (alg == PERM_ALG_BATCH_PARTITION && cplx && m > 5) alg = (n >= 9) ? PERM_ALG_GLYNN : PERM_ALG_RYSER;
+  }
   if (n > 16 && !(alg == PERM_ALG_GLYNN && n <= kWalkMultiMaxN) &&
-      !(alg == PERM_ALG_BATCH_PARTITION && n <= 62 && m <= (cplx ? 4 : 6))) {
+      !(alg == PERM_ALG_BATCH_PARTITION && n <= 62 && m <= (cplx ? 5 : 6))) {
     set_error("batched kernels handle n <= 16 (Glynn: n <= 30; the partition formula, m <= 6: n <= 62); "
               "use the single-permanent entry points");
     return PERM_BAD_SHAPE;

@@ -83,12 +83,12 @@ cudaError_t launch_laplace8(const void* a, void* out, int64_t B, cudaStream_t s)
 }
 
 // (M, N), 1 <= M <= 6, M <= N <= 16: IDX = (M-1)*16 + (N-1); f64 needs even
-// N (16-byte row chunks); complex stops at M = 4 (the 2^M complex subset sums
-// would not fit in registers)
+// N (16-byte row chunks); complex stops at M = 5 (M = 6: the 64 complex
+// subset sums spill)
 template <typename T, int I>
 bulk_fn part_entry() {
   constexpr int M = I / 16 + 1, N = I % 16 + 1;
-  if constexpr (N >= M && (sizeof(T) == 16 ? M <= 4 : N % 2 == 0)) return &launch_partition<T, M, N>;
+  if constexpr (N >= M && (sizeof(T) == 16 ? M <= 5 : N % 2 == 0)) return &launch_partition<T, M, N>;
   else return nullptr;
 }
 template <typename T, int... Is>
@@ -117,10 +117,10 @@ rt_fn pick_rt(int m, std::integer_sequence<int, Ms...>) {
 // Partition formula for wide rectangles, 16 < n <= 62 (m <= 6 real, m <= 4
 // complex): runtime-n kernel (no bulk staging).
 int launch_partition_wide(bool cplx, int64_t B, int m, int n, const void* dA, void* dOut, cudaStream_t stream) {
-  rt_fn fn = cplx ? pick_rt<cd>(m, std::make_integer_sequence<int, 4>{})
+  rt_fn fn = cplx ? pick_rt<cd>(m, std::make_integer_sequence<int, 5>{})
                   : pick_rt<double>(m, std::make_integer_sequence<int, 6>{});
   if (!fn || n > 62 || m > n) {
-    set_error("the partition batch formula covers m <= 6 (complex m <= 4), n <= 62");
+    set_error("the partition batch formula covers m <= 6 (complex m <= 5), n <= 62");
     return PERM_BAD_SHAPE;
   }
   const cudaError_t e = fn(dA, dOut, B, n, stream);
@@ -130,7 +130,7 @@ int launch_partition_wide(bool cplx, int64_t B, int m, int n, const void* dA, vo
 bool bulk_batch_supported(int alg, bool cplx, int m, int n) {
   if (alg == PERM_ALG_BATCH_LAPLACE) return !cplx && m == 8 && n == 8;
   if (alg == PERM_ALG_BATCH_PARTITION)
-    return m >= 1 && m <= n && n <= 16 && (cplx ? m <= 4 : (m <= 6 && n % 2 == 0));
+    return m >= 1 && m <= n && n <= 16 && (cplx ? m <= 5 : (m <= 6 && n % 2 == 0));
   return false;
 }
 
@@ -143,7 +143,7 @@ int launch_bulk_batch(int alg, bool cplx, int64_t B, int m, int n, const void* d
   if (alg == PERM_ALG_BATCH_LAPLACE) {
     fn = &launch_laplace8;
   } else {
-    fn = cplx ? pick_partition<cd>(m, n, std::make_integer_sequence<int, 64>{})
+    fn = cplx ? pick_partition<cd>(m, n, std::make_integer_sequence<int, 80>{})
               : pick_partition<double>(m, n, std::make_integer_sequence<int, 96>{});
   }
   if (!fn) return -1;

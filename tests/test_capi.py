@@ -121,8 +121,8 @@ def test_no_cpu_fallback_without_gpu():
 
 def test_batch_shape_contracts_without_gpu():
     """Shape validation of the batch entry points happens before any device
-    work, so it is exercised here: the partition formula stops at m = 6 and
-    n = 62 (complex beyond n = 16: m <= 4), the Laplace formula is 8x8 only,
+    work, so it is exercised here: the partition formula stops at m = 6
+    (complex m = 5) and n = 62, the Laplace formula is 8x8 only,
     Glynn batches stop at n = 30, the other algorithms at n = 16."""
     import numpy as np
 
@@ -141,4 +141,4 @@ def test_batch_shape_contracts_without_gpu():
     with pytest.raises(ValueError):
         P.partition_batch(np.zeros((2, 5, 63)))  # 62 columns at most
     with pytest.raises(ValueError):
-        P.partition_batch(np.zeros((2, 5, 20)) + 0j)  # complex wide rectangles: m <= 4
+        P.partition_batch(np.zeros((2, 6, 20)) + 0j)  # complex: m <= 5
