@@ -155,6 +155,33 @@ def cpu_walk_rate_fixed(O, a, steps, nthreads):
 
 # ------------------------------------------------------------- engine arm
 def run_engine(args):
+    # stdout carries the JSON line only: under torchrun, NCCL prints its
+    # version banner to the process's stdout (NCCL_DEBUG=VERSION is set in
+    # the GPU image), so file descriptor 1 points at stderr for the run and
+    # the JSON line is written to the saved descriptor
+    json_fd = None
+    if "WORLD_SIZE" in os.environ:
+        sys.stdout.flush()
+        json_fd = os.dup(1)
+        os.dup2(2, 1)
+    try:
+        return _run_engine(args, json_fd)
+    finally:
+        if json_fd is not None:
+            sys.stdout.flush()
+            os.dup2(json_fd, 1)
+            os.close(json_fd)
+
+
+def _emit(line: dict, json_fd):
+    text = json.dumps(line)
+    if json_fd is None:
+        print(text, flush=True)
+    else:
+        os.write(json_fd, (text + "\n").encode())
+
+
+def _run_engine(args, json_fd):
     import torch
     import torch.distributed as dist
 
@@ -329,7 +356,7 @@ def run_engine(args):
             "gpu_launches": args.steps,  # one walk_kernel per step (block partials combined in-kernel)
             "clocks": clocks,
         }
-        print(json.dumps(line))
+        _emit(line, json_fd)
     if distributed:
         dist.barrier()
         dist.destroy_process_group()
