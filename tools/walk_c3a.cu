@@ -43,8 +43,8 @@ void run(int B, int r) {
   cudaFree(d); cudaFree(parts); cudaFree(dn);
 }
 int main() {
-  for (int b : {13, 15, 17, 19, 21, 23}) run<double, 24>(b, 0);
-  for (int b : {13, 17, 19, 21, 23}) run<cd, 24>(b, 0);
-  for (int b : {19, 21, 23, 25}) run<double, 36>(b, 0);
+  for (int r : {0, 4, 5, 6, 7, 8, 9, 10}) run<double, 26>(25, r);
+  for (int r : {0, 5, 6, 7, 8, 9, 10}) run<double, 28>(27, r);
+  for (int r : {0, 4, 5, 6, 7, 8}) run<double, 22>(21, r);
   return 0;
 }
