@@ -2,6 +2,7 @@
 // launch shape: the small-walk end of the walk kernel (latency-bound).
 #include <cstdio>
 #include <random>
+#include <string>
 #include <vector>
 #include "../paper_2510_03421_b200/csrc/walk_launch.cuh"
 using namespace permb200;
@@ -42,9 +43,22 @@ void run(int B, int r) {
          plan.log2L, plan.grid, kWalkThreads, ms, ops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d); cudaFree(parts); cudaFree(dn);
 }
-int main() {
-  for (int r : {0, 4, 5, 6, 7, 8, 9, 10}) run<double, 26>(25, r);
-  for (int r : {0, 5, 6, 7, 8, 9, 10}) run<double, 28>(27, r);
-  for (int r : {0, 4, 5, 6, 7, 8}) run<double, 22>(21, r);
+// modes: (none) C3a chunk sweep; "floor" small-walk floor; "lsweep" chunk
+// length sweep at P = 22, 26, 28 (the cost model's check)
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "";
+  if (mode == "floor") {
+    for (int b : {13, 15, 17, 19, 21, 23}) run<double, 24>(b, 0);
+    for (int b : {13, 17, 19, 21, 23}) run<cd, 24>(b, 0);
+    for (int b : {19, 21, 23, 25}) run<double, 36>(b, 0);
+  } else if (mode == "lsweep") {
+    for (int r : {0, 4, 5, 6, 7, 8, 9, 10}) run<double, 26>(25, r);
+    for (int r : {0, 5, 6, 7, 8, 9, 10}) run<double, 28>(27, r);
+    for (int r : {0, 4, 5, 6, 7, 8}) run<double, 22>(21, r);
+  } else {
+    for (int r : {0, 3, 4, 5, 6, 7}) run<cd, 24>(23, r);
+    for (int r : {0, 4, 5, 6}) run<double, 24>(23, r);
+    for (int r : {0, 4, 5, 6}) run<double, 26>(25, r);
+  }
   return 0;
 }
