@@ -159,17 +159,28 @@ static int launch_walk_multi_batch(bool cplx, int64_t B, int m, int n, const voi
   static int bps_cache[2][kWalkMultiMaxN + 1] = {};  // benign race: idempotent
   int& bps = bps_cache[cplx ? 1 : 0][n];
   if (!bps) bps = bfn();
-  const WalkMultiPlan pl = plan_walk_multi(n, B, nsm, bps);
-  const size_t part_bytes = (size_t)B * pl.segs * kPartialStride * sizeof(double);
-  const size_t done_bytes = ((size_t)B * sizeof(unsigned int) + 255) & ~(size_t)255;
-  void* scratch = nullptr;
-  PERM_CUDA_TRY(cudaMallocAsync(&scratch, part_bytes + done_bytes, stream));
-  unsigned int* done = static_cast<unsigned int*>(scratch);
-  double* partials = reinterpret_cast<double*>(static_cast<char*>(scratch) + done_bytes);
-  cudaError_t e = cudaMemsetAsync(done, 0, (size_t)B * sizeof(unsigned int), stream);
-  if (e == cudaSuccess) e = fn(dA, dOut, B, m, partials, done, pl, stream);
-  const cudaError_t ef = cudaFreeAsync(scratch, stream);
-  if (e == cudaSuccess) e = ef;
+  // at most 2^20 matrices per launch: bounded scratch (partials + counters)
+  // however large the device-resident batch
+  constexpr int64_t kMaxPerLaunch = 1 << 20;
+  const int esz = cplx ? 16 : 8;
+  cudaError_t e = cudaSuccess;
+  for (int64_t b0 = 0; b0 < B && e == cudaSuccess; b0 += kMaxPerLaunch) {
+    const int64_t nb = std::min<int64_t>(kMaxPerLaunch, B - b0);
+    const WalkMultiPlan pl = plan_walk_multi(n, nb, nsm, bps);
+    const size_t part_bytes = (size_t)nb * pl.segs * kPartialStride * sizeof(double);
+    const size_t done_bytes = ((size_t)nb * sizeof(unsigned int) + 255) & ~(size_t)255;
+    void* scratch = nullptr;
+    e = cudaMallocAsync(&scratch, part_bytes + done_bytes, stream);
+    if (e != cudaSuccess) break;
+    unsigned int* done = static_cast<unsigned int*>(scratch);
+    double* partials = reinterpret_cast<double*>(static_cast<char*>(scratch) + done_bytes);
+    e = cudaMemsetAsync(done, 0, (size_t)nb * sizeof(unsigned int), stream);
+    if (e == cudaSuccess)
+      e = fn(static_cast<const char*>(dA) + (size_t)b0 * m * n * esz, static_cast<char*>(dOut) + (size_t)b0 * esz,
+             nb, m, partials, done, pl, stream);
+    const cudaError_t ef = cudaFreeAsync(scratch, stream);
+    if (e == cudaSuccess) e = ef;
+  }
   return e == cudaSuccess ? PERM_OK : cuda_fail(e, "batched walk launch");
 }
 
