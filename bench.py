@@ -153,6 +153,23 @@ def cpu_walk_rate_fixed(O, a, steps, nthreads):
     return time.perf_counter() - t
 
 
+def check_value(n: int, v: float) -> dict:
+    """Self-check of the benchmarked result against the committed GPU
+    double-double Ryser value (tests/golden/c5_dd.json): fail loudly when
+    the relative error exceeds 1e-10, or the scale-aware metric (ii) does."""
+    ref = json.loads((ROOT / "tests" / "golden" / "c5_dd.json").read_text())
+    dd = ref["ryser_dd"].get(str(n))
+    if dd is None:
+        return {"value": v, "checked": False}
+    rel = abs(v - dd) / max(abs(v), abs(dd))
+    M = ref["glynn_magsum"].get(str(n), abs(dd))
+    scaled = abs(v - dd) / max(abs(v), abs(dd), M)
+    if rel > 1e-10 or scaled > 1e-10:
+        raise SystemExit(f"bench: C5 n={n} value {v!r} differs from the double-double Ryser {dd!r} "
+                         f"(rel {rel:.3e}, scaled {scaled:.3e})")
+    return {"value": v, "checked": True, "ref_ryser_dd": dd, "rel_err": rel, "scaled_err": scaled}
+
+
 # ------------------------------------------------------------- engine arm
 def run_engine(args):
     # stdout carries the JSON line only: under torchrun, NCCL prints its
@@ -232,6 +249,7 @@ def _run_engine(args, json_fd):
         step()
     torch.cuda.synchronize()
     value_check, _ = finish("glynn", a, gathered.cpu().numpy())
+    check = check_value(n, value_check)
 
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
@@ -239,19 +257,35 @@ def _run_engine(args, json_fd):
     if distributed:
         dist.barrier()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
     kernel_ms = []
     for i in range(args.steps):
         flush.fill_(float(i))  # > 126 MB L2, outside the timed events
         ev[i][0].record(stream)
-        step()
-        ev[i][1].record(stream)
+        gpu_partial("glynn", a, k0, k1, False, device_out=part, stream=stream.cuda_stream)
+        ev[i][1].record(stream)  # walk done: [1] -> [2] is the exchange
+        if distributed:
+            dist.all_gather_into_tensor(gathered, part)
+        else:
+            gathered.copy_(part)
+        ev[i][2].record(stream)
         kernel_ms.append(lib.perm_last_kernel_ms())
     torch.cuda.synchronize()
+    # per-rank breakdown (walk kernel, walk call, exchange), gathered to rank 0
+    mine = torch.tensor([statistics.mean(kernel_ms), statistics.mean(s.elapsed_time(m) for s, m, _ in ev),
+                         statistics.mean(m.elapsed_time(e) for _, m, e in ev), float(k1 - k0)],
+                        dtype=torch.float64, device="cuda")
+    per_rank = torch.zeros(4 * world, dtype=torch.float64, device="cuda")
+    if distributed:
+        dist.all_gather_into_tensor(per_rank, mine)
+    else:
+        per_rank.copy_(mine)
+    per_rank = [dict(zip(("walk_kernel_ms", "walk_call_ms", "exchange_ms", "gray_steps"), map(float, r)))
+                for r in per_rank.view(world, 4).cpu().tolist()]
     if distributed:
         dist.barrier()
     clocks = sampler.stop() if sampler else None
-    t_ms = sum(s.elapsed_time(e) for s, e in ev)
+    t_ms = sum(s.elapsed_time(e) for s, _, e in ev)
     t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
     if distributed:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -334,13 +368,17 @@ def _run_engine(args, json_fd):
                        "parallelism": f"gray-range shards x{world} (NCCL all-gather of 8-double partials)",
                        "l2": "flushed (256 MiB write) before every step, outside the timed events",
                        "launch": {"grid": grid.value, "threads": 256, "log2_chunk": log2L.value},
-                       "value_check": value_check,
+                       "value_check": check,
+                       "per_rank": per_rank,
                        "n_sweep_1gpu": sweep},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_pipe, "unit": "FP64 op/s",
                          "frac": achieved / peak_pipe, "frac_of_fma_peak": achieved / peak_dfma,
                          "frac_of_nominal": achieved / NOMINAL_DFMA,
                          "peak_dfma": peak_dfma, "peak_dadd_dmul": peak_addmul,
                          "traffic": traffic,
+                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch from the "
+                                           "committed ncu --set full capture (profiles/roofline_traffic.json), "
+                                           "not measured in this run",
                          "peak_source": "measured live on this GPU, max of two FP64-pipe probes "
                                         "(perm_fp64_pipe_probe: DFMA chains, DADD/DMUL chains); "
                                         "MEASURED_PEAKS.json has no FP64 entry; nominal = 148 SM x 64 "

@@ -256,9 +256,10 @@ def walk_f64_mt(setup, k0=0, k1=None, nthreads=None):
     return float(out[0]) + float(out[1])
 
 
-def walk_dd_mt(setup, k0=0, k1=None, nthreads=None):
+def walk_dd_mt(setup, k0=0, k1=None, nthreads=None, mag=False):
     """Double-double walk sum over [k0, k1): returns (hi, lo) pairs
-    ((re_hi, re_lo), (im_hi, im_lo))."""
+    ((re_hi, re_lo), (im_hi, im_lo)); with ``mag`` also the raw magnitude
+    sum sum_k |w_k term_k| (dd-accumulated, rounded)."""
     L = lib()
     nthreads = nthreads or os.cpu_count() or 1
     k1 = (1 << setup["B"]) if k1 is None else k1
@@ -267,9 +268,11 @@ def walk_dd_mt(setup, k0=0, k1=None, nthreads=None):
     v0 = np.ascontiguousarray(setup["v0"], dt)
     U = np.ascontiguousarray(setup["U"], dt)
     w = np.array(setup["w"] or [0.0], np.float64)
-    out = np.zeros(4)
+    out = np.zeros(6)
     L.orc_walk_mt(1, setup["P"], setup["B"], int(cplx), int(setup["weighted"]), v0.ctypes.data,
                   U.ctypes.data, w.ctypes.data, k0, k1, nthreads, out.ctypes.data)
+    if mag:
+        return (out[0], out[1]), (out[2], out[3]), out[4] + out[5]
     return (out[0], out[1]), (out[2], out[3])
 
 
@@ -335,13 +338,27 @@ def prescale_factor(a: np.ndarray) -> float:
     return float(2.0 ** round(-math.log2(rms)))
 
 
-def glynn_magnitude_sum(a: np.ndarray, scale=None) -> float:
-    """M = norm * sum_k |prod_j colsum_j(k)|, by brute
-    walk in numpy (small n only)."""
+def ryser_magnitude_sum(a: np.ndarray, nthreads=None) -> float:
+    """Ryser's magnitude sum sum_S |w_S prod_i rowsum_i(S)| (the all-subsets
+    form, double-double walk): the scale for Ryser of a permanent that is
+    exactly 0, where Glynn's M can vanish while Ryser leaves O(eps M_R)."""
+    a = as_array(a)
+    a = a.astype(np.complex128 if np.iscomplexobj(a) else np.float64)
+    _, _, mg = walk_dd_mt(walk_setup(RYSER, a), nthreads=nthreads, mag=True)
+    return float(mg)
+
+
+def glynn_magnitude_sum(a: np.ndarray, scale=None, nthreads=None) -> float:
+    """M = norm * sum_k |prod_j colsum_j(k)|: by brute
+    walk in numpy for n <= 14, else the C double-double walk (threads)."""
     a = as_array(a)
     m, n = a.shape
     if scale is None:
         scale = prescale_factor(a) if m < n else 1.0
+    if n > 14:
+        s = walk_setup(GLYNN, a.astype(np.complex128 if np.iscomplexobj(a) else np.float64), scale=scale)
+        _, _, mg = walk_dd_mt(s, nthreads=nthreads, mag=True)
+        return float(mg / (2.0 ** (n - 1) * math.factorial(n - m) * scale ** m))
     full = np.ones((n, n), np.complex128 if np.iscomplexobj(a) else np.float64)
     full[:m] = a * scale
     K = 1 << (n - 1)

@@ -692,11 +692,15 @@ static inline cdd cdd_mul(cdd a, cdd b) {
 
 /* double-double range walk, real (cplx = 0) or complex (cplx = 1; v0/U/w
  * interleaved re,im).  The state is re-seeded exactly (in dd) at k0, so
- * colsum drift is at the dd level.  out: [re_hi, re_lo, im_hi, im_lo]. */
+ * colsum drift is at the dd level.  out: [re_hi, re_lo, im_hi, im_lo,
+ * mag_hi, mag_lo], mag = sum_k |w_k| |term_k| (the raw magnitude sum behind
+ * the scale of SURVEY 8(c) metric (ii); |complex| from the dd parts rounded
+ * to double). */
 void orc_walk_dd_range(int P, int B, int is_cplx, const double* v0, const double* U,
                        int weighted, const double* w, uint64_t k0, uint64_t k1, double* out) {
   cdd v[64];
   cdd total = {{0, 0}, {0, 0}};
+  dd mag = {0, 0};
   uint64_t g0 = k0 ^ (k0 >> 1);
   int st = is_cplx ? 2 : 1;
   for (int j = 0; j < P; ++j) {
@@ -735,8 +739,11 @@ void orc_walk_dd_range(int P, int B, int is_cplx, const double* v0, const double
       total = cdd_add(total, p);
     } else if (k & 1) total = cdd_sub(total, p);
     else total = cdd_add(total, p);
+    if (is_cplx) mag = dd_add(mag, dd_from(hypot(p.re.hi + p.re.lo, p.im.hi + p.im.lo)));
+    else mag = dd_add(mag, p.re.hi < 0 ? dd_neg(p.re) : p.re);
   }
   out[0] = total.re.hi; out[1] = total.re.lo; out[2] = total.im.hi; out[3] = total.im.lo;
+  out[4] = mag.hi; out[5] = mag.lo;
 }
 
 /* Wrapping int128 range walk (mod 2^128 ring arithmetic).
@@ -776,7 +783,7 @@ typedef struct {
   const void *v0, *U, *w;
   uint64_t k0, k1;
   double f64_out;
-  double dd_out[4];
+  double dd_out[6];
   uint64_t i128_out[2];
 } job_t;
 
@@ -820,12 +827,15 @@ void orc_walk_mt(int kind, int P, int B, int is_cplx, int weighted, const void* 
     ((double*)out)[0] = s.hi; ((double*)out)[1] = s.lo;
   } else if (kind == 1) {
     cdd s = {{0, 0}, {0, 0}};
+    dd mg = {0, 0};
     for (int i = 0; i < nthreads; ++i) {
       cdd x = {{jobs[i].dd_out[0], jobs[i].dd_out[1]}, {jobs[i].dd_out[2], jobs[i].dd_out[3]}};
       s = cdd_add(s, x);
+      dd y = {jobs[i].dd_out[4], jobs[i].dd_out[5]};
+      mg = dd_add(mg, y);
     }
-    double* o = (double*)out;
-    o[0] = s.re.hi; o[1] = s.re.lo; o[2] = s.im.hi; o[3] = s.im.lo;
+    double* o = (double*)out;  /* 6 doubles */
+    o[0] = s.re.hi; o[1] = s.re.lo; o[2] = s.im.hi; o[3] = s.im.lo; o[4] = mg.hi; o[5] = mg.lo;
   } else {
     u128 s = 0;
     for (int i = 0; i < nthreads; ++i) s += ((u128)jobs[i].i128_out[1] << 64) | jobs[i].i128_out[0];

@@ -105,7 +105,7 @@ int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, 
   st = load_matrix(m, n, a, lda, dev_ptr, cplx, &A, stream);
   if (st) return st;
   WalkSetup ws;
-  st = build_walk(alg, A, &ws);
+  st = build_walk(alg, A, &ws, /*exact_state=*/true);
   if (st) return st;
   Scratch* s = scratch();
   if (!s) return cuda_fail(cudaErrorNoDevice, "scratch");
@@ -142,7 +142,7 @@ int walk_partial(int alg, bool cplx, int m, int n, const double* a, int64_t lda,
   st = load_matrix(m, n, a, lda, dev_ptr, cplx, &A, stream);
   if (st) return st;
   WalkSetup ws;
-  st = build_walk(alg, A, &ws);
+  st = build_walk(alg, A, &ws, /*exact_state=*/true);
   if (st) return st;
   Scratch* s = scratch();
   if (!s) return cuda_fail(cudaErrorNoDevice, "scratch");

@@ -146,7 +146,33 @@ static inline double binom_d(int a, int b) {
   return (double)(long double)r;
 }
 
-int build_walk(int alg, const HostMat& A, WalkSetup* ws) {
+// Exact walk state (DESIGN 2.1 "Exact state"): every state component of a
+// walk is a signed subset sum of one column (Glynn: sum_i d_i a_ij) or one
+// row (Ryser: sum_{j in S} a_ij), bounded by c = sum |entries| of it.  Round
+// each entry of that column / row to the grid q = 2^(e - 52), c <= 2^e: then
+// every partial sum is an integer multiple of q below 2^52 q, so seeds and all
+// 2^B in-place updates are exact and the state never drifts.  The matrix
+// moves by <= q/2 per entry, the same size as one FP64 rounding of the column
+// sums the walk already forms (<= c 2^-52); a CPU study
+// (tools/chunk_drift_exp.c, profiles/r2_chunk_drift.txt) puts the drift
+// of the unquantized walk at 30-100x the error this leaves.  Real and
+// imaginary parts get their own grids.  Integer-valued matrices are already
+// on every grid q <= 1 and stay bit-identical.
+static void quantize_line(double* x, size_t count, size_t stride, const std::vector<size_t>& keep_exact) {
+  long double c = 0;
+  for (size_t k = 0; k < count; ++k) c += std::fabs((long double)x[k * stride]);
+  if (!(c > 0) || !std::isfinite((double)c)) return;
+  int e = 0;
+  std::frexp((double)c * (1.0 + 4e-16), &e);  // c <= 2^e (margin for the long double -> double cast)
+  const int qe = std::max(e - 52, -1074);
+  for (size_t k : keep_exact) {  // ones rows of rectangular Glynn must stay on the grid
+    const double r = std::ldexp(std::nearbyint(std::ldexp(x[k * stride], -qe)), qe);
+    if (r != x[k * stride]) return;
+  }
+  for (size_t k = 0; k < count; ++k) x[k * stride] = std::ldexp(std::nearbyint(std::ldexp(x[k * stride], -qe)), qe);
+}
+
+int build_walk(int alg, const HostMat& A, WalkSetup* ws, bool exact_state) {
   const int m = A.m, n = A.n;
   const int w = A.cplx ? 2 : 1;
   ws->cplx = A.cplx;
@@ -162,8 +188,23 @@ int build_walk(int alg, const HostMat& A, WalkSetup* ws) {
     ws->v0_off = 0;
     ws->U_off = (size_t)n * w;
     ws->buf.assign((size_t)n * w + (size_t)(n - 1) * n * w, 0.0);
-    auto row_re = [&](int i, int j) { return i < m ? std::ldexp(A.re(i, j), s) : 1.0; };
-    auto row_im = [&](int i, int j) { return i < m ? std::ldexp(A.im(i, j), s) : 0.0; };
+    // the walked matrix: real rows scaled by 2^s, ones rows below
+    std::vector<double> G((size_t)n * n * w);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        G[((size_t)i * n + j) * w] = i < m ? std::ldexp(A.re(i, j), s) : 1.0;
+        if (w == 2) G[((size_t)i * n + j) * w + 1] = i < m ? std::ldexp(A.im(i, j), s) : 0.0;
+      }
+    if (exact_state) {
+      std::vector<size_t> ones;
+      for (int i = m; i < n; ++i) ones.push_back((size_t)i);
+      for (int j = 0; j < n; ++j) {
+        quantize_line(&G[(size_t)j * w], (size_t)n, (size_t)n * w, ones);
+        if (w == 2) quantize_line(&G[(size_t)j * w + 1], (size_t)n, (size_t)n * w, {});
+      }
+    }
+    auto row_re = [&](int i, int j) { return G[((size_t)i * n + j) * w]; };
+    auto row_im = [&](int i, int j) { return G[((size_t)i * n + j) * w + 1]; };
     for (int j = 0; j < n; ++j) {
       // exactly-rounded column sums (long double accumulation)
       long double sr = 0, si = 0;
@@ -203,6 +244,10 @@ int build_walk(int alg, const HostMat& A, WalkSetup* ws) {
         double c = binom_d(n - s, m - s);
         ws->buf[ws->w_off + s] = ((m - s) & 1) ? -c : c;
       }
+    if (exact_state)  // state component i = row i's subset sum: U[t][i] over t
+      for (int i = 0; i < m; ++i)
+        for (int part = 0; part < w; ++part)
+          quantize_line(&ws->buf[ws->U_off + (size_t)i * w + part], (size_t)n, (size_t)m * w, {});
     return PERM_OK;
   }
   set_error("unknown algorithm");

@@ -66,7 +66,10 @@ struct WalkSetup {
   size_t v0_off = 0, U_off = 0, w_off = 0;  // offsets in doubles
   int wlen = 0;
 };
-int build_walk(int alg, const HostMat& A, WalkSetup* ws);
+// exact_state: round each state line (Glynn column / Ryser row) to a grid on
+// which every walk state is exact (the float walks; not the double-double
+// validation walks, which see the matrix as given).
+int build_walk(int alg, const HostMat& A, WalkSetup* ws, bool exact_state = false);
 // Power-of-two pre-scale exponent for rectangular Glynn: round(-log2(RMS|a|)).
 int prescale_log2(const HostMat& A);
 // Normalize a raw walk sum (re, im, mag) into the permanent.

@@ -117,3 +117,19 @@ def test_prescaled_rect_glynn_is_well_conditioned(rng):
     ref = O.permanent("combinatoric", a)[0]
     v = O.dd_permanent("glynn", a, nthreads=4)
     assert abs(v - ref) <= 1e-12 * abs(ref)
+
+
+def test_magnitude_sum_two_restatements_agree(rng):
+    """The scale M of metric (ii) has two oracle restatements: the numpy
+    brute walk (n <= 14) and the C double-double walk's |term| sum (used
+    above 14 columns).  They agree to 1e-13 on square, rectangular and
+    complex shapes, so the GPU tests' M pin (test_gpu_parity.py
+    test_engine_magsum_pinned_to_oracle) is anchored in both."""
+    shapes = [(12, 12, False), (9, 14, True), (5, 13, False), (14, 14, True), (1, 6, False)]
+    for m, n, cplx in shapes:
+        a = rng.uniform(-1, 1, (m, n)) + (1j * rng.uniform(-1, 1, (m, n)) if cplx else 0)
+        brute = O.glynn_magnitude_sum(a)
+        sc = O.prescale_factor(a) if m < n else 1.0
+        _, _, mg = O.walk_dd_mt(O.walk_setup("glynn", a, scale=sc), nthreads=2, mag=True)
+        viac = mg / (2.0 ** (n - 1) * math.factorial(n - m) * sc ** m)
+        assert abs(brute - viac) <= 1e-13 * brute, (m, n, cplx, brute, viac)
