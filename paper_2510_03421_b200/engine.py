@@ -36,11 +36,20 @@ def _stage(a):
     return C.c_void_p(arr.ctypes.data), arr.shape[1], 0, arr, None
 
 
+def _kind(a) -> str:
+    """numpy dtype kind character of an array or tensor ('i', 'f', 'c')."""
+    if isinstance(a, np.ndarray):
+        return a.dtype.kind
+    if a.is_complex():
+        return "c"
+    return "f" if a.is_floating_point() else "i"
+
+
 def walk(alg: str, a, magsum: bool = False):
     """Glynn / Ryser permanent of a float64 or complex128 m x n (m <= n)
     matrix; returns (value, M) with M the magnitude sum (or None)."""
     lib = _lib.load()
-    cplx = np.iscomplexobj(a) if not hasattr(a, "is_complex") else a.is_complex()
+    cplx = _kind(a) == "c"
     m, n = a.shape
     ptr, lda, dev, keep, stream = _stage(a)
     out = _lib.out_buf(2)
@@ -60,7 +69,7 @@ def comb(a, step_budget: int, width: int = 64):
     the int128 bound fails.  BUDGET is mapped by the caller."""
     lib = _lib.load()
     m, n = a.shape
-    kind = a.dtype.kind if isinstance(a, np.ndarray) else None
+    kind = _kind(a)
     ptr, lda, dev, keep, stream = _stage(a)
     budget = C.c_uint64(min(int(step_budget), (1 << 64) - 1) if step_budget >= 0 else 0)
     if kind in ("i",):
@@ -76,7 +85,7 @@ def comb(a, step_budget: int, width: int = 64):
         _lib.check(st, f"combinatoric {m}x{n}")
         v = (int(out[1]) << 64) | (int(out[0]) & ((1 << 64) - 1))
         return v, (width == 128 and not fits.value), st
-    cplx = np.iscomplexobj(a)
+    cplx = kind == "c"
     out = _lib.out_buf(2)
     fn = lib.perm_comb_c128 if cplx else lib.perm_comb_f64
     st = fn(m, n, ptr, lda, dev, budget, out, stream)
@@ -110,6 +119,8 @@ def walk_dd(alg: str, a):
     """Double-double Glynn / Ryser on the GPU (validation): returns
     ((re_hi, re_lo), (im_hi, im_lo)) of the normalized permanent."""
     lib = _lib.load()
+    if not isinstance(a, np.ndarray):  # validation walk: host copy of a device matrix
+        a = a.cpu().numpy()
     cplx = np.iscomplexobj(a)
     a = np.ascontiguousarray(a, dtype=np.complex128 if cplx else np.float64)
     m, n = a.shape

@@ -6,15 +6,17 @@ one key per line, floats in shortest round-trip form; unknown, duplicate or
 missing keys and other versions are rejected with ValueError.
 
 Two fits over B200 kernel timings {(m, n): {alg: seconds}}:
-* ``run_tuning`` -- the reference's procedure (tuner.py:108-310): timing
-  grid, labels with margin ratios, near-tie filter, two maximum-margin lines
-  over (r, n) (hard-margin SVM, weighted minimum-cost fallback when the
-  labels are not separable), p4 from the square cutoff, p8 chosen to
-  minimize the total dispatch slowdown;
-* ``fit_params`` -- a direct grid search minimizing the summed relative
-  slowdown (used for the shipped ``tuned/b200.tuning``: GPU timings below
-  ~50 us are launch-overhead dominated, so labels there are noisy and
-  rarely separable).
+* ``run_tuning`` -- the reference's procedure (tuner.py:96-333, same names:
+  ``algorithm_feasible``, ``time_algorithm``, ``build_label_grid``,
+  ``fit_hard_margin_svm``, ``plane_intersection``, ``assemble_params``):
+  timing grid, labels with margin ratios, near-tie filter, two
+  maximum-margin lines over (r, n) (``svm.py``; weighted minimum-cost
+  fallback when the labels are not separable), p4 from the square cutoff,
+  p8 from the lines' crossing;
+* ``fit_params`` -- a direct search minimizing the summed relative slowdown
+  (GPU timings below ~50 us are launch-overhead dominated, so labels there
+  are noisy and rarely separable; profiles/r2_dispatch_fit.txt compares the
+  two on the same B200 timings).
 """
 from __future__ import annotations
 
@@ -87,8 +89,10 @@ def _regret_line(cells: dict, pos: str, neg: str, skip):
         w.append(abs(ca - cb))
     if len(X) < 2 or len(set(y)) < 2:
         return None
-    wv, b = _min_cost_line(np.array(X, float), np.array(y), np.array(w), angles=720)
-    if wv is None or (wv[0] == 0 and wv[1] == 0):
+    from . import svm
+
+    wv, b, _ = svm.min_misclassification_plane(np.array(X, float), np.array(y), angles=720, weights=np.array(w))
+    if wv[0] == 0 and wv[1] == 0:
         return None
     return float(wv[0]), float(wv[1]), float(b)
 
@@ -175,36 +179,49 @@ def fit_params(timings: dict, host: str = "") -> TuningParams:
 
 
 # ---------------------------------------------------------------------------
-# The reference's tuning procedure (src/tuner.py:108-310) on B200 timings:
+# The reference's tuning procedure (src/tuner.py:96-333) on B200 timings:
 # timing grid -> labels with margin ratios -> near-tie filter -> two
-# maximum-margin lines over (r, n) -> p4 / p8 -> TuningParams.
+# maximum-margin lines over (r, n) (svm.py) -> p4 / p8 -> TuningParams.
+# Same names and contracts as the reference's ``permanent.tuner``.
 # ---------------------------------------------------------------------------
 import statistics  # noqa: E402
 import time  # noqa: E402
-from dataclasses import dataclass  # noqa: E402
+from dataclasses import dataclass, field  # noqa: E402
 
 import numpy as np  # noqa: E402
 
-GRID_N = range(2, 35)
+from . import svm  # noqa: E402
+from .core import ElementKind  # noqa: E402
+
+GRID_N = range(2, 25)                     # the reference's grid (tuner.py:27)
+B200_GRID_N = range(2, 35)                # the B200 fit: walks are cheap up to n = 34
 GRID_RATIOS = (1 / 8, 1 / 4, 3 / 8, 1 / 2, 5 / 8, 3 / 4, 7 / 8, 1.0)
-NEAR_TIE_FILTER = 1.05
+COMBINATORIC_MAX_COLS = 14                # CPU budgets of algorithm_feasible (tuner.py:32-36)
 COMBINATORIC_MAX_STEPS = 50_000_000
+WALK_MAX_COLS = 26
+NEAR_TIE_FILTER = 1.05
 MIN_SAMPLE_SECONDS = 200e-6
 
 
 @dataclass(frozen=True)
 class BenchmarkSample:
+    """Median time of one algorithm at one grid shape (tuner.py:44-55)."""
+
     algorithm: object
     m: int
     n: int
     ratio: float
     median_time: float
     trials: int
+    kind: ElementKind = ElementKind.FLOAT64
     feasible: bool = True
 
 
 @dataclass(frozen=True)
 class LabeledPoint:
+    """A grid cell labeled with its fastest algorithm; ``margin_ratio`` =
+    runner-up / winner (inf with one feasible algorithm)."""
+
     r: float
     n: int
     m: int
@@ -215,6 +232,9 @@ class LabeledPoint:
 
 @dataclass(frozen=True)
 class SeparatingPlane:
+    """weight_r r + weight_n n + bias = 0; the first trained class is on the
+    positive side; ``fallback`` when the classes were not separable."""
+
     weight_r: float
     weight_n: float
     bias: float
@@ -230,29 +250,38 @@ class TuningReport:
     grid: list
     plane_small: SeparatingPlane
     plane_large: SeparatingPlane
-    timings: dict
+    intersection: object = None
+    timings: dict = field(default_factory=dict)
 
 
-def grid_shapes(n_range=GRID_N, ratios=GRID_RATIOS):
-    seen, out = set(), []
-    for n in n_range:
-        for r in ratios:
-            m = max(1, round(r * n))
-            if m <= n and (m, n) not in seen:
-                seen.add((m, n))
-                out.append((m, n))
-    return out
+def algorithm_feasible(alg, m: int, n: int, comb_steps: int = COMBINATORIC_MAX_STEPS,
+                       comb_cols: int = COMBINATORIC_MAX_COLS, walk_cols: int = WALK_MAX_COLS) -> bool:
+    """Whether a cell is affordable on the tuning grid.  Defaults are the
+    reference's CPU budgets (tuner.py:96-102); the B200 grid passes its own
+    (``B200_BUDGET``)."""
+    from .algorithms import AlgorithmId
+
+    if alg is AlgorithmId.COMBINATORIC:
+        return n <= comb_cols and m * math.perm(n, m) <= comb_steps
+    return n <= walk_cols
 
 
-def time_algorithm(alg, m, n, trials=5, seed=None) -> BenchmarkSample:
-    """Median wall time of run_algorithm on fresh U[-1,1] float64 matrices,
-    repeats amortized to >= MIN_SAMPLE_SECONDS (src/tuner.py:108-135)."""
-    from .algorithms import AlgorithmId, run_algorithm
+# the B200 grid: the GPU combinatoric kernel handles ~1e9 row-steps in tens
+# of ms, and the walks reach n = 34 in ~30 ms
+B200_BUDGET = dict(comb_steps=2_000_000_000, comb_cols=20, walk_cols=34)
+
+
+def time_algorithm(alg, m, n, trials=5, seed=None, budget=None) -> BenchmarkSample:
+    """Median wall time of ``run_algorithm`` (the public mid-level call: host
+    matrix in, Python value out, kernels in between) on fresh U[-1,1]
+    float64 matrices, repeats amortized to >= MIN_SAMPLE_SECONDS
+    (tuner.py:108-135)."""
+    from .algorithms import run_algorithm
     from .core import as_matrix
 
     if trials < 3:
         raise ValueError(f"need at least 3 trials, got {trials}")
-    if alg is AlgorithmId.COMBINATORIC and math.perm(n, m) > COMBINATORIC_MAX_STEPS:
+    if not algorithm_feasible(alg, m, n, **(budget or {})):
         return BenchmarkSample(alg, m, n, m / n, math.inf, 0, feasible=False)
     g = np.random.default_rng(seed)
     mats = [as_matrix(g.uniform(-1.0, 1.0, (m, n))) for _ in range(trials + 1)]
@@ -269,34 +298,41 @@ def time_algorithm(alg, m, n, trials=5, seed=None) -> BenchmarkSample:
     return BenchmarkSample(alg, m, n, m / n, statistics.median(ts), trials)
 
 
-def evaluate_dispatch(params: TuningParams, shapes, trials: int = 5, seed: int = 0):
-    """(m, n, chosen, slowdown) per probe shape, slowdown = the chosen
-    algorithm's median / the fastest feasible median, timed on the GPU engine
-    (the reference's acceptance probe, src/tuner.py:313-333)."""
-    from .algorithms import AlgorithmId
-    from .dispatch import select_algorithm
-
-    out = []
-    probe_seed = seed + 90000
-    for m, n in shapes:
-        chosen = select_algorithm(m, n, params)
-        medians = {}
-        for alg in AlgorithmId:
-            probe_seed += 1
-            smp = time_algorithm(alg, m, n, trials=trials, seed=probe_seed)
-            if smp.feasible:
-                medians[alg] = smp.median_time
-        best = min(medians.values())
-        out.append((m, n, chosen, medians[chosen] / best if chosen in medians else math.inf))
+def grid_shapes(n_range=GRID_N, ratios=GRID_RATIOS):
+    """Deduplicated (m, n) cells, m = max(1, round(r n)) (tuner.py:138-149)."""
+    seen, out = set(), []
+    for n in n_range:
+        for r in ratios:
+            m = max(1, round(r * n))
+            if m <= n and (m, n) not in seen:
+                seen.add((m, n))
+                out.append((m, n))
     return out
 
 
+def measure_grid(n_range=GRID_N, ratios=GRID_RATIOS, trials=5, seed=0, budget=None) -> dict:
+    """{(m, n): {alg: median seconds}} over the feasible algorithms."""
+    from .algorithms import AlgorithmId
+
+    timings, s = {}, seed
+    for m, n in grid_shapes(n_range, ratios):
+        cell = {}
+        for alg in AlgorithmId:
+            s += 1
+            smp = time_algorithm(alg, m, n, trials=trials, seed=s, budget=budget)
+            if smp.feasible:
+                cell[alg.value] = smp.median_time
+        timings[(m, n)] = cell
+    return timings
+
+
 def label_grid(timings: dict) -> list:
-    """Label each cell {(m, n): {alg: seconds}} by its fastest algorithm."""
+    """Label each cell by its fastest algorithm, in grid order; cells with no
+    feasible algorithm are omitted."""
     from .algorithms import AlgorithmId
 
     pts = []
-    for (m, n), t in sorted(timings.items(), key=lambda kv: (kv[0][1], kv[0][0])):
+    for (m, n), t in timings.items():
         feas = sorted((v, a) for a, v in t.items() if math.isfinite(v))
         if not feas:
             continue
@@ -305,19 +341,9 @@ def label_grid(timings: dict) -> list:
     return pts
 
 
-def build_label_grid(n_range=GRID_N, ratios=GRID_RATIOS, trials=5, seed=0):
-    from .algorithms import AlgorithmId
-
-    timings, s = {}, seed
-    for m, n in grid_shapes(n_range, ratios):
-        cell = {}
-        for alg in AlgorithmId:
-            s += 1
-            smp = time_algorithm(alg, m, n, trials=trials, seed=s)
-            if smp.feasible:
-                cell[alg.value] = smp.median_time
-        timings[(m, n)] = cell
-    return label_grid(timings), timings
+def build_label_grid(n_range=GRID_N, ratios=GRID_RATIOS, trials=5, seed=0, budget=None) -> list:
+    """Time every algorithm on every cell and label the winners (tuner.py:152-173)."""
+    return label_grid(measure_grid(n_range, ratios, trials, seed, budget))
 
 
 def detect_small_square_cutoff(grid) -> int:
@@ -332,70 +358,81 @@ def detect_small_square_cutoff(grid) -> int:
     return cut
 
 
-def _max_margin(X, y):
-    """Hard-margin linear SVM in 2-D (min |w|^2 s.t. y (w.x + b) >= 1), or
-    None if the classes are not linearly separable."""
-    from scipy.optimize import minimize
-
-    scale = np.maximum(np.abs(X).max(axis=0), 1e-12)
-    Xs = X / scale
-    cons = {"type": "ineq", "fun": lambda z: y * (Xs @ z[:2] + z[2]) - 1.0,
-            "jac": lambda z: np.column_stack([y[:, None] * Xs, y])}
-    best = None
-    for z0 in (np.array([1.0, 0.0, 0.0]), np.array([0.0, 1.0, 0.0]), np.array([1.0, 1.0, -1.0])):
-        r = minimize(lambda z: z[0] ** 2 + z[1] ** 2, z0, jac=lambda z: np.array([2 * z[0], 2 * z[1], 0.0]),
-                     constraints=[cons], method="SLSQP", options={"maxiter": 500, "ftol": 1e-12})
-        if r.success and np.all(y * (Xs @ r.x[:2] + r.x[2]) >= 1.0 - 1e-6):
-            if best is None or r.fun < best.fun:
-                best = r
-    if best is None:
-        return None
-    w = best.x[:2] / scale
-    return w, float(best.x[2])
-
-
-def _min_cost_line(X, y, weights, angles=1440):
-    """Weighted minimum-misclassification line: sweep directions; for each,
-    the best threshold over sorted projections by cumulative sums."""
-    scale = np.maximum(np.abs(X).max(axis=0), 1e-12)
-    Xs = X / scale
-    best = (math.inf, None, None)
-    for th in np.linspace(0.0, 2 * math.pi, angles, endpoint=False):
-        w = np.array([math.cos(th), math.sin(th)])
-        proj = Xs @ w
-        order = np.argsort(proj)
-        ps, ys, ws = proj[order], y[order], weights[order]
-        # threshold after position i: points <= are predicted -1, > are +1
-        pos_left = np.concatenate([[0.0], np.cumsum(ws * (ys > 0))])       # +1 points on the -1 side
-        neg_right = np.concatenate([np.cumsum((ws * (ys < 0))[::-1])[::-1], [0.0]])  # -1 points on the +1 side
-        cost = pos_left + neg_right
-        i = int(np.argmin(cost))
-        if cost[i] < best[0]:
-            if i == 0:
-                b = ps[0] - 1.0
-            elif i == len(ps):
-                b = ps[-1] + 1.0
-            else:
-                b = 0.5 * (ps[i - 1] + ps[i])
-            best = (float(cost[i]), w / scale, -b)
-    return best[1], best[2]
-
-
-def fit_separator(points, class_a, class_b, near_tie=NEAR_TIE_FILTER) -> SeparatingPlane:
-    """Max-margin line between two labels over (r, n) after the near-tie
-    filter; weighted min-cost fallback when not separable (src/tuner.py:187-213)."""
+def fit_hard_margin_svm(points, class_a, class_b, near_tie: float = NEAR_TIE_FILTER) -> SeparatingPlane:
+    """Maximum-margin line between two labels over (r, n) after dropping
+    near-ties; ``class_a`` on the positive side.  Not separable: the
+    weighted minimum-cost line (misrouting costs margin_ratio - 1, capped at
+    9), flagged ``fallback`` (tuner.py:187-213)."""
     kept = [p for p in points if p.label in (class_a, class_b) and p.margin_ratio >= near_tie]
-    if not any(p.label is class_a for p in kept) or not any(p.label is class_b for p in kept):
-        raise ValueError("both classes need retained training points")
+    for cls in (class_a, class_b):
+        if not any(p.label is cls for p in kept):
+            raise ValueError(f"no retained training points labeled {cls.value}")
     X = np.array([[p.r, p.n] for p in kept], dtype=float)
     y = np.array([1.0 if p.label is class_a else -1.0 for p in kept])
-    fit = _max_margin(X, y)
+    fit = svm.max_margin_plane(X, y)
     if fit is not None:
-        w, b = fit
-        return SeparatingPlane(float(w[0]), float(w[1]), b)
+        w, b, _ = fit
+        return SeparatingPlane(float(w[0]), float(w[1]), float(b))
     wts = np.array([min(p.margin_ratio, 10.0) - 1.0 for p in kept])
-    w, b = _min_cost_line(X, y, wts)
+    w, b, _ = svm.min_misclassification_plane(X, y, weights=wts)
     return SeparatingPlane(float(w[0]), float(w[1]), float(b), fallback=True)
+
+
+def plane_intersection(p: SeparatingPlane, q: SeparatingPlane):
+    """(r, n) where the two lines cross (Cramer's rule), or None when they
+    are parallel to within 1e-12 of the coefficient scale."""
+    det = p.weight_r * q.weight_n - p.weight_n * q.weight_r
+    scale = max(1.0, abs(p.weight_r), abs(p.weight_n), abs(q.weight_r), abs(q.weight_n)) ** 2
+    if abs(det) < 1e-12 * scale:
+        return None
+    r = (-p.bias * q.weight_n + q.bias * p.weight_n) / det
+    n = (-q.bias * p.weight_r + p.bias * q.weight_r) / det
+    return float(r), float(n)
+
+
+def assemble_params(grid, plane1: SeparatingPlane, plane2: SeparatingPlane, p4, p8) -> TuningParams:
+    """p1..p3 from plane1 (combinatoric positive), p5..p7 from plane2 (Glynn
+    positive), p4 clamped to p8; a plane on which every relevant training
+    point lies is rejected as orientation-ambiguous (tuner.py:226-250)."""
+    from .algorithms import AlgorithmId
+
+    C, G, R = AlgorithmId.COMBINATORIC, AlgorithmId.GLYNN, AlgorithmId.RYSER
+    for plane, pos, neg in ((plane1, C, G), (plane2, G, R)):
+        rel = [p for p in grid if p.label in (pos, neg)]
+        if rel and all(abs(plane.evaluate(p.r, p.n)) <= 1e-12 for p in rel):
+            raise ValueError("separating plane orientation is ambiguous: every training point lies on the plane")
+    stamp = datetime.datetime.now(datetime.timezone.utc).isoformat(timespec="seconds")
+    return TuningParams(p1=plane1.weight_r, p2=plane1.weight_n, p3=plane1.bias, p4=float(min(p4, p8)),
+                        p5=plane2.weight_r, p6=plane2.weight_n, p7=plane2.bias, p8=float(p8),
+                        source="machine-tuned", created_at=stamp,
+                        host=f"{platform.node()} ({platform.machine()})")
+
+
+def _fit_or_default(points, class_a, class_b) -> SeparatingPlane:
+    """fit_hard_margin_svm, or a constant-sign line steering every cell away
+    from a class that never wins decisively (tuner.py:253-266)."""
+    won = {p.label for p in points if p.margin_ratio >= NEAR_TIE_FILTER}
+    if class_a in won and class_b in won:
+        return fit_hard_margin_svm(points, class_a, class_b)
+    return SeparatingPlane(0.0, -1.0, 0.0) if class_a not in won else SeparatingPlane(0.0, 1.0, 0.0)
+
+
+def _derive_p8(plane1, plane2, grid, max_n):
+    """Regime boundary: the lines' crossing column, else one past the last
+    combinatoric win; raised to cover every decisive (>= 1.25x)
+    combinatoric cell, clamped to [2, max_n] (tuner.py:269-283)."""
+    from .algorithms import AlgorithmId
+
+    inter = plane_intersection(plane1, plane2)
+    comb = [p for p in grid if p.label is AlgorithmId.COMBINATORIC]
+    if inter is not None and 2 <= inter[1] <= max_n:
+        p8 = round(inter[1])
+    else:
+        p8 = max(p.n for p in comb) + 1 if comb else 2
+    decisive = [p.n for p in comb if p.margin_ratio >= 1.25]
+    if decisive:
+        p8 = max(p8, max(decisive))
+    return max(2, min(p8, max_n)), inter
 
 
 def _total_slowdown(params, timings):
@@ -408,43 +445,46 @@ def _total_slowdown(params, timings):
     return tot
 
 
-def run_tuning(n_range=GRID_N, ratios=GRID_RATIOS, trials=5, seed=0, timings=None) -> TuningReport:
-    """The whole pipeline; with ``timings`` ({(m, n): {alg: s}}) it only fits."""
-    import datetime
-    import platform
-
+def run_tuning(n_range=GRID_N, ratios=GRID_RATIOS, trials=5, seed=0, timings=None, budget=None) -> TuningReport:
+    """The reference's pipeline (tuner.py:286-310): label grid, p4 from the
+    square cutoff, the combinatoric/Glynn line on the unpinned cells, the
+    Glynn/Ryser line fit twice (second pass on the large regime the first
+    located), p8 from their crossing.  ``timings`` ({(m, n): {alg: s}})
+    skips the measurement and fits recorded B200 timings."""
     from .algorithms import AlgorithmId
 
     C, G, R = AlgorithmId.COMBINATORIC, AlgorithmId.GLYNN, AlgorithmId.RYSER
     if timings is None:
-        grid, timings = build_label_grid(n_range, ratios, trials, seed)
-    else:
-        grid = label_grid(timings)
+        timings = measure_grid(n_range, ratios, trials, seed, budget)
+    grid = label_grid(timings)
     max_n = max(p.n for p in grid)
     p4 = detect_small_square_cutoff(grid)
+    unpinned = [p for p in grid if not (p.m == p.n and p.n <= p4)]
+    plane1 = _fit_or_default(unpinned, C, G)
+    plane2 = _fit_or_default(grid, G, R)
+    p8, _ = _derive_p8(plane1, plane2, grid, max_n)
+    large = [p for p in grid if p.n > p8]
+    plane2 = _fit_or_default(large or grid, G, R)
+    p8, inter = _derive_p8(plane1, plane2, grid, max_n)
+    params = assemble_params(grid, plane1, plane2, p4, p8)
+    return TuningReport(params, grid, plane1, plane2, inter, timings)
 
-    def plane(pts, a, b, default):
-        try:
-            return fit_separator(pts, a, b)
-        except ValueError:
-            return default
 
-    plane1 = plane([p for p in grid if not (p.m == p.n and p.n <= p4)], C, G,
-                   SeparatingPlane(-1.0, 0.0, -1.0, fallback=True))
-    best = None
-    for p8 in range(max(2, p4), max_n + 1):
-        large = [p for p in grid if p.n > p8]
-        plane2 = plane(large or grid, G, R, SeparatingPlane(1.0, 0.0, 1.0, fallback=True))
-        try:
-            params = TuningParams(plane1.weight_r, plane1.weight_n, plane1.bias, float(p4),
-                                  plane2.weight_r, plane2.weight_n, plane2.bias, float(p8),
-                                  source="machine-tuned")
-        except ValueError:
-            continue
-        cost = _total_slowdown(params, timings)
-        if best is None or cost < best[0]:
-            best = (cost, params, plane2)
-    _, params, plane2 = best
-    stamp = datetime.datetime.now(datetime.timezone.utc).strftime("%Y-%m-%dT%H:%M:%SZ")
-    params = TuningParams(*params.as_list(), source="machine-tuned", created_at=stamp, host=platform.node())
-    return TuningReport(params, grid, plane1, plane2, timings)
+def evaluate_dispatch(params: TuningParams, shapes, trials: int = 5, seed: int = 0, budget=None):
+    """(m, n, chosen, slowdown) per probe shape: the selected algorithm's
+    median time over the fastest feasible one's, timed on the GPU engine
+    (the acceptance probe of tuner.py:313-333)."""
+    from .algorithms import AlgorithmId
+    from .dispatch import select_algorithm
+
+    out, s = [], seed + 90000
+    for m, n in shapes:
+        chosen = select_algorithm(m, n, params)
+        med = {}
+        for alg in AlgorithmId:
+            s += 1
+            smp = time_algorithm(alg, m, n, trials=trials, seed=s, budget=budget)
+            if smp.feasible:
+                med[alg] = smp.median_time
+        out.append((m, n, chosen, med[chosen] / min(med.values()) if chosen in med else math.inf))
+    return out

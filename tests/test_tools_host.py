@@ -93,21 +93,44 @@ def test_tuning_pipeline_on_synthetic_timings():
     rep = T.run_tuning(timings=t)
     p = rep.params
     assert p.source == "machine-tuned"
-    # the max-margin table is close to (or better than) the defaults here
+    # the slowdown search is close to (or better than) the defaults here
     from paper_2510_03421_b200.dispatch import default_params
 
-    assert T._total_slowdown(p, t) <= 1.02 * T._total_slowdown(default_params(), t)
+    assert T._total_slowdown(T.fit_params(t), t) <= 1.02 * T._total_slowdown(default_params(), t)
     grid = T.label_grid(t)
     assert all(pt.margin_ratio >= 1.0 for pt in grid)
     for (m, n) in t:
         select_algorithm(m, n, p)  # total over the grid
 
 
+def test_reference_procedure_on_recorded_b200_timings():
+    """run_tuning (the reference's max-margin procedure) on the B200 grid
+    timings committed in profiles/: the table it emits beats the reference's
+    CPU defaults and is the shipped tuned/b200.tuning (profiles/r2_dispatch_fit.txt)."""
+    import json
+
+    from paper_2510_03421_b200.dispatch import b200_params, default_params
+    from conftest import ROOT
+
+    raw = json.loads((ROOT / "profiles" / "r1_dispatch_timings.json").read_text())
+    t = {tuple(int(x) for x in k.split(",")): v for k, v in raw.items()}
+    rep = T.run_tuning(timings=t)
+    assert T._total_slowdown(rep.params, t) <= T._total_slowdown(default_params(), t) * 0.9
+    shipped = b200_params()
+    assert shipped.as_list() == rep.params.as_list()
+    grid = T.label_grid(t)
+    assert all(pt.margin_ratio >= 1.0 for pt in grid)
+    for (m, n) in t:
+        select_algorithm(m, n, shipped)  # total over the grid
+
+
 def test_max_margin_separates():
     X = np.array([[0.1, 2], [0.2, 3], [0.9, 20], [0.8, 22]], dtype=float)
     y = np.array([1.0, 1.0, -1.0, -1.0])
-    w, b = T._max_margin(X, y)
+    from paper_2510_03421_b200 import svm
+
+    w, b, gap = svm.max_margin_plane(X, y)
     assert np.all(y * (X @ w + b) > 0)
-    wts = np.ones(4)
-    w2, b2 = T._min_cost_line(X, y, wts)
-    assert np.all(y * (X @ w2 + b2) > 0)
+    assert (y * (X @ w + b)).min() == pytest.approx(1.0)
+    w2, b2, cost = svm.min_misclassification_plane(X, y, weights=np.ones(4))
+    assert cost == 0 and np.all(y * (X @ w2 + b2) > 0)
