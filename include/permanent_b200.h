@@ -91,6 +91,17 @@ int perm_ryser_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, doub
 int perm_ryser_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
                     void* stream);
 
+/* The reference's rectangular Ryser kernel for any m <= n, square included
+ * (permanent_ryser_rectangular accepts m == n, src/algorithms.py:118-137;
+ * ryser_rect / ryser_rect_int, src/_kernels.py:226-365): subset sizes
+ * s = m..1 in lexicographic combination order, weights (-1)^(m-s) C(n-s, m-s).
+ * n up to 256 columns (the reference caps only its Gray walks at 62).
+ * i64 = checked int64, PERM_OVERFLOW exactly where ryser_rect_int reports
+ * overflow; out[0], out[1] = low, high 64 bits. */
+int perm_ryser_rect_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, void* stream);
+int perm_ryser_rect_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, void* stream);
+int perm_ryser_rect_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int64_t* out, void* stream);
+
 /* ---- combinatoric (src/_kernels.py:28-56, 59-108; src/algorithms.py:71-90)
  * Depth-first enumeration of the m-permutations with prefix products and
  * zero pruning, the DFS tree split at a prefix depth across threads.
@@ -111,7 +122,7 @@ int perm_comb_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int 
  * width = 64: the reference's checked-int64 semantics bit for bit
  *   (glynn_sq_int / glynn_rect_int / ryser_sq_int / ryser_rect_int,
  *   src/_kernels.py:148-365, 412-697, and the exact-division checks of
- *   src/algorithms.py:431-461): PERM_OVERFLOW exactly when the reference
+ *   src/algorithms.py:150-181): PERM_OVERFLOW exactly when the reference
  *   reports overflowed=True (its OverflowError, src/__init__.py:43-47).
  * width = 128: exact permanent via a mod-2^128 walk, certified to fit by an
  *   FP64 run and its magnitude-sum error bound; PERM_OVERFLOW if the

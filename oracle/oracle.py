@@ -89,7 +89,7 @@ def _kind(a: np.ndarray) -> str:
 
 
 def as_array(a) -> np.ndarray:
-    """The reference's dtype mapping (src/core.py:152-158, 252-275)."""
+    """The reference's dtype mapping (src/core.py:29-47, 141-164)."""
     arr = np.asarray(a)
     k = arr.dtype.kind
     dt = {"b": np.int64, "i": np.int64, "u": np.int64, "f": np.float64, "c": np.complex128}[k]
@@ -175,7 +175,7 @@ def permanent(alg: str, a, step_budget: int = 2_000_000_000, compiled=None):
             # numba hands back a Python complex, whose division by a float
             # is componentwise true division; the interpreted kernel's numpy
             # complex128 divides by multiplying with the reciprocal -- the two
-            # modes differ in the last bit here (src/algorithms.py:462-463)
+            # modes differ in the last bit here (src/algorithms.py:182-183)
             acc = complex(acc)
         value = acc / (2.0 ** (n - 1)) / float(math.factorial(n - m))
         return _plain(value, kind), False

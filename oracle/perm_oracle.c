@@ -250,7 +250,7 @@ static void ryser_weights_f64(int m, int n, double* w) {
   }
 }
 
-/* ryser_rect: src/_kernels.py:226-262; weights as src/algorithms.py:410-416. */
+/* ryser_rect: src/_kernels.py:226-262; weights as src/algorithms.py:110-115. */
 double orc_ryser_rect_f64(int m, int n, const double* a) {
   double w[65];
   ryser_weights_f64(m, n, w);
@@ -331,7 +331,7 @@ void orc_ryser_rect_c128(int m, int n, const double* a_, double* out) {
 }
 
 /* ryser_rect_int: src/_kernels.py:265-365 (weights always fit int64 for
- * n <= 62, so the src/algorithms.py:410-411 guard never fires). */
+ * n <= 62, so the src/algorithms.py:129-130 guard never fires). */
 int orc_ryser_rect_i64(int m, int n, const int64_t* a, int64_t* out) {
   int64_t w[65];
   for (int s = 1; s <= m; ++s) {

@@ -40,6 +40,9 @@ SIGNATURES = {
     "perm_glynn_c128": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _dp, _vp]),
     "perm_ryser_f64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _dp, _vp]),
     "perm_ryser_c128": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _dp, _vp]),
+    "perm_ryser_rect_f64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _vp]),
+    "perm_ryser_rect_c128": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _vp]),
+    "perm_ryser_rect_i64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _ip, _vp]),
     "perm_comb_f64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_uint64, _dp, _vp]),
     "perm_comb_c128": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_uint64, _dp, _vp]),
     "perm_comb_i64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, C.c_uint64, _ip,

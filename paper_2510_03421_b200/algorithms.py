@@ -89,12 +89,32 @@ def permanent_ryser_square(a: Matrix, compiled=None, exact=None) -> PermanentRes
     return _float_result(engine.walk("ryser", a.data)[0], a.kind)
 
 
+#: columns of the combination-ordered kernels (csrc/comb.cuh kCombMaxN); the
+#: reference's ryser_rect and combinatoric have no column cap
+_MAX_COMB_COLS = 256
+
+
 def permanent_ryser_rectangular(a: Matrix, compiled=None, exact=None) -> PermanentResult:
-    """Binomial-weighted Ryser for m <= n (src/algorithms.py:118-137)."""
+    """Binomial-weighted Ryser for m <= n, square included (src/algorithms.py:118-137).
+
+    Integers keep the reference's checked-int64 semantics of ryser_rect_int:
+    the lexicographic combination order runs for every m <= n (the square
+    Gray walk of ``permanent_ryser_square`` checks other intermediates, so
+    its overflow flag could differ near the int64 onset).  Floats take the
+    popcount-weighted Gray walk up to 62 columns (or the combination order
+    where it is cheaper), and the combination order past 62 columns."""
     _need(a.m <= a.n, f"need m <= n, got {a.m}x{a.n}; transpose first")
-    _need(a.n <= _MAX_ENUM_COLS, f"subset walk over {a.n} columns exceeds 2^62 steps")
+    _need(a.m <= _MAX_ENUM_COLS and a.n <= _MAX_COMB_COLS,
+          f"rectangular Ryser supports m <= {_MAX_ENUM_COLS}, n <= {_MAX_COMB_COLS}; got {a.m}x{a.n}")
     if a.kind is ElementKind.INT64:
-        return _int_walk("ryser", a, exact)
+        if exact == "int128" and a.n <= _MAX_ENUM_COLS:
+            return _int_walk("ryser", a, exact)
+        if exact not in _EXACT_MODES:
+            raise ValueError(f"exact must be one of {_EXACT_MODES}, got {exact!r}")
+        value, ovf = engine.ryser_rect(a.data)
+        return PermanentResult(int(value), bool(ovf))
+    if a.n > _MAX_ENUM_COLS:
+        return _float_result(engine.ryser_rect(a.data)[0], a.kind)
     return _float_result(engine.walk("ryser", a.data)[0], a.kind)
 
 

@@ -66,6 +66,7 @@ int check_shape(int alg, int m, int n) {
 // rectangular shapes despite its heavier per-step update.
 bool ryser_rect_use_comb(int m, int n) {
   if (m >= n) return false;
+  if (n > 62) return true;
   long double c = 0, b = 1;  // running C(n, s)
   for (int s = 1; s <= m; ++s) {
     b = b * (n - s + 1) / s;
@@ -78,10 +79,12 @@ bool ryser_rect_use_comb(int m, int n) {
 int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out,
                 double* magsum, void* stream_) {
   clear_error();
+  // very rectangular Ryser (and any width past the walks' 62 columns, where
+  // the reference's ryser_rect has no cap): the reference's combination order
+  if (alg == PERM_ALG_RYSER && magsum == nullptr && m >= 1 && m < n && ryser_rect_use_comb(m, n))
+    return comb_permanent(true, cplx ? 1 : 0, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream_);
   int st = check_shape(alg, m, n);
   if (st) return st;
-  if (alg == PERM_ALG_RYSER && magsum == nullptr && ryser_rect_use_comb(m, n))
-    return comb_permanent(true, cplx ? 1 : 0, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream_);
   // walks shorter than one warp-group of chunks (Glynn n <= 8, Ryser n <= 7):
   // the register-resident thread-per-matrix batch kernels, batch of one
   if (magsum == nullptr && !dev_ptr && lda == n && walk_steps(alg, m, n) < 256) {
@@ -540,6 +543,26 @@ int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int
     return PERM_OK;
   }
   return int_permanent(PERM_ALG_RYSER, m, n, a, lda, dev_ptr, width, out, fits_int64, stream);
+}
+
+// The reference's ryser_rect kernels for any m <= n, square included
+// (src/algorithms.py:118-137 accepts m == n; src/_kernels.py:226-365): the
+// lexicographic combination order, so the checked-int64 overflow flag of
+// ryser_rectangular(square) is the reference's (the square Gray walk checks
+// other intermediates).
+int perm_ryser_rect_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, void* stream) {
+  return comb_permanent(true, 0, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream);
+}
+int perm_ryser_rect_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, void* stream) {
+  return comb_permanent(true, 1, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream);
+}
+int perm_ryser_rect_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int64_t* out, void* stream) {
+  int64_t v = 0;
+  int st = comb_permanent(true, 2, m, n, a, lda, dev_ptr, UINT64_MAX, nullptr, &v, stream);
+  if (st) return st;
+  out[0] = v;
+  out[1] = v < 0 ? -1 : 0;
+  return PERM_OK;
 }
 
 int perm_comb_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t step_budget, double* out,

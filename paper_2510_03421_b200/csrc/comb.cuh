@@ -21,12 +21,18 @@
 namespace permb200 {
 
 constexpr int kCombThreads = 128;
+// Column limit of the combination-ordered kernels.  The reference caps only
+// its Gray walks at 62 columns (src/algorithms.py:47); its combinatoric and
+// rectangular Ryser take any width (work P(n, m), sum_{s<=m} C(n, s)), so
+// these kernels index columns up to kCombMaxN; rows stay <= 62.
+constexpr int kCombMaxN = 256;
+constexpr int kBinomCols = 64;  // binomial table C(i, j): i <= kCombMaxN, j < 64, saturating
 
 enum CombMode { kCombF64 = 0, kCombC128 = 1, kCombI64 = 2, kCombI128 = 3 };
 
 struct CombArgs {
   const void* a;          // m x n row-major (double / cd / int64)
-  const uint64_t* binom;  // [63][63] binomial table C(i, j)
+  const uint64_t* binom;  // [kCombMaxN + 1][kBinomCols] binomial table C(i, j)
   int m, n, s;            // ryser: subset size s
   uint64_t total;         // number of items (combinations / prefixes)
   uint64_t per_thread;    // items per thread
@@ -41,7 +47,7 @@ struct CombArgs {
 };
 
 __device__ __forceinline__ uint64_t binom_at(const uint64_t* tab, int i, int j) {
-  return (j < 0 || j > i || i < 0) ? 0ull : tab[i * 63 + j];
+  return (j < 0 || j > i || i < 0) ? 0ull : tab[i * kBinomCols + j];
 }
 
 // ---------------------------------------------------------------- Ryser
@@ -66,7 +72,7 @@ __global__ void __launch_bounds__(kCombThreads) ryser_comb_kernel(CombArgs A) {
                                        typename std::conditional<MODE == kCombC128, cd, int64_t>::type>::type;
   extern __shared__ __align__(16) unsigned char comb_smem[];
   const uint64_t* bt = A.binom;
-  int bstride = 63;
+  int bstride = kBinomCols;
   const Te* abase = static_cast<const Te*>(A.a);
   {
     unsigned char* p = comb_smem;
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
   for (uint64_t pidx = p0; pidx < p1 && !sm.flag; ++pidx) {
     // decode prefix: mixed radix (n, n-1, ..., n-D+1), most significant first
     int choice[64];
-    bool used[64];
+    bool used[kCombMaxN];
     for (int j = 0; j < n; ++j) used[j] = false;
     {
       uint64_t rem = pidx;

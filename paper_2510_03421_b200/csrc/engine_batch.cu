@@ -533,6 +533,21 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
   BatchPipe& bp = batch_pipe();
   int st = bp.ensure(in_chunk, out_chunk);
   if (st) return st;
+  // Results parked in a slot belong to the call that parked them: drop any
+  // left behind by an earlier call that returned early, and drop ours on
+  // every early return below, so no later call copies stale results into
+  // its own (possibly shorter) output.
+  struct SlotReset {
+    BatchPipe& bp;
+    void drop() {
+      for (int slot = 0; slot < 2; ++slot) {
+        cudaEventSynchronize(bp.done[slot]);
+        bp.pending[slot] = 0;
+      }
+    }
+    ~SlotReset() { drop(); }
+  } slot_reset{bp};
+  slot_reset.drop();
   for (int64_t c0 = 0, it = 0; c0 < B; c0 += chunk, ++it) {
     const int slot = (int)(it & 1);
     const int64_t cnt = std::min<int64_t>(chunk, B - c0);

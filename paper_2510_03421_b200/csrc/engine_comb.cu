@@ -19,15 +19,20 @@ static uint64_t nperm(int n, int k) {  // P(n, k), saturating
 }
 
 static const std::vector<uint64_t>& binom_table() {
-  static std::vector<uint64_t> t;
-  if (t.empty()) {
-    t.assign(63 * 63, 0);
-    for (int i = 0; i < 63; ++i) {
-      t[i * 63] = 1;
-      for (int j = 1; j <= i; ++j) t[i * 63 + j] = t[(i - 1) * 63 + j - 1] + (j <= i - 1 ? t[(i - 1) * 63 + j] : 0);
+  static const std::vector<uint64_t> table = [] {  // thread-safe one-time init
+    std::vector<uint64_t> t;
+    const int R = kCombMaxN + 1, W = kBinomCols;
+    t.assign((size_t)R * W, 0);
+    for (int i = 0; i < R; ++i) {
+      t[(size_t)i * W] = 1;
+      for (int j = 1; j <= i && j < W; ++j) {  // saturating Pascal rule
+        const uint64_t x = t[(size_t)(i - 1) * W + j - 1], y = (j <= i - 1) ? t[(size_t)(i - 1) * W + j] : 0;
+        t[(size_t)i * W + j] = (x > UINT64_MAX - y) ? UINT64_MAX : x + y;
+      }
     }
-  }
-  return t;
+    return t;
+  }();
+  return table;
 }
 
 static int device_binom_table(const uint64_t** out) {
@@ -103,7 +108,7 @@ static int enqueue_ryser_fused(const void* dA, const uint64_t* dB, int m, int n,
   a.fused = 1;
   uint64_t off = 0;
   for (int s = m; s >= 1; --s) {
-    const uint64_t total = bt[n * 63 + s];
+    const uint64_t total = bt[(size_t)n * kBinomCols + s];
     uint64_t per = (total + thr - 1) / thr;
     if (per < 1) per = 1;
     const uint64_t blocks = ((total + per - 1) / per + kCombThreads - 1) / kCombThreads;
@@ -176,9 +181,19 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
     set_error("matrix must have m >= 1 and n >= 1");
     return PERM_BAD_SHAPE;
   }
-  if (m > n || n > 62) {
-    set_error(m > n ? "need m <= n; transpose first" : "more than 62 columns");
+  if (m > n || n > kCombMaxN || m > 62) {
+    set_error(m > n ? "need m <= n; transpose first"
+                    : (m > 62 ? "more than 62 rows" : "more than kCombMaxN = 256 columns"));
     return PERM_BAD_SHAPE;
+  }
+  if (ryser) {  // sum_{s<=m} C(n, s) combinations, counted in uint64 ranks
+    const auto& bt0 = binom_table();
+    unsigned __int128 tot = 0;
+    for (int s = 1; s <= m; ++s) tot += bt0[(size_t)n * kBinomCols + s];
+    if (tot > ((unsigned __int128)1 << 62)) {
+      set_error("combination-order Ryser over more than 2^62 column subsets");
+      return PERM_BUDGET;
+    }
   }
   if (!ryser) {  // src/algorithms.py:78-84
     const uint64_t perms = nperm(n, m);
@@ -247,7 +262,7 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
     st = fetch_partials(dOut, off, &all, stream);
     if (st) return st;
     for (int s = m; s >= 1 && !ovf; --s) {
-      int64_t c = (int64_t)bt[(n - s) * 63 + (m - s)];
+      int64_t c = (int64_t)bt[(size_t)(n - s) * kBinomCols + (m - s)];  // <= C(n, m) < 2^62 (checked above)
       const int64_t w = ((m - s) & 1) ? -c : c;
       h.assign(all.begin() + first[s] * 8, all.begin() + (first[s] + cnt[s]) * 8);
       if (mode == 2) {

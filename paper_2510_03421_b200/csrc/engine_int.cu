@@ -460,7 +460,7 @@ static int int_finish(int alg, const IntPlan& pl, int width, const IntPart* part
     }
     s128 v = (int64_t)T;
     if (alg == PERM_ALG_GLYNN) {
-      if (v % pl.denom != 0) {  // src/algorithms.py:436-437, 459-460
+      if (v % pl.denom != 0) {  // src/algorithms.py:155-157, 178-180
         set_error("Glynn sum not divisible by its normalization");
         return PERM_OVERFLOW;
       }

@@ -136,3 +136,24 @@ def walk_steps(alg: str, m: int, n: int) -> int:
 
 def sm_count() -> int:
     return int(_lib.load().perm_device_sm_count())
+
+
+def ryser_rect(a):
+    """The reference's ryser_rect kernel (lexicographic combination order,
+    any m <= n incl. square, n <= 256): (value, overflowed); integers with
+    the reference's checked int64 flag (src/_kernels.py:226-365)."""
+    lib = _lib.load()
+    m, n = a.shape
+    kind = _kind(a)
+    ptr, lda, dev, keep, stream = _stage(a)
+    if kind == "i":
+        out = (C.c_int64 * 2)()
+        st = lib.perm_ryser_rect_i64(m, n, ptr, lda, dev, out, stream)
+        if st == _lib.OVERFLOW:
+            return 0, True
+        _lib.check(st, f"ryser_rect {m}x{n}")
+        return int(out[0]), False
+    out = _lib.out_buf(2)
+    fn = lib.perm_ryser_rect_c128 if kind == "c" else lib.perm_ryser_rect_f64
+    _lib.check(fn(m, n, ptr, lda, dev, out, stream), f"ryser_rect {m}x{n}")
+    return (complex(out[0], out[1]) if kind == "c" else float(out[0])), False

@@ -167,6 +167,19 @@ def _sharded_int(a, alg, group, exact, partial_fn):
     a = np.ascontiguousarray(a, dtype=np.int64)
     m, n = a.shape
     rank, world, backend = _world(group)
+    if alg == "ryser" and m < n and exact is None and partial_fn is None:
+        # the checked-int64 flag of rectangular Ryser belongs to the
+        # reference's sequential combination order (ryser_rect_int,
+        # src/_kernels.py:265-365), not to a Gray range: every rank evaluates
+        # it whole (combination-order kernel, sum_{s<=m} C(n, s) subsets --
+        # the cheap form for the very rectangular shapes it is chosen for);
+        # exact="int128" shards the Gray walk instead
+        from . import engine
+
+        value, ovf = engine.ryser_rect(a)
+        if ovf:
+            raise OverflowError("rectangular Ryser: an int64 intermediate overflowed (reference semantics)")
+        return int(value)
     k0, k1 = shard_range(alg, m, n, rank, world)
     if partial_fn is not None:
         part = torch.tensor(np.asarray(partial_fn(alg, a, k0, k1), dtype=np.int64))

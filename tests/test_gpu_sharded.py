@@ -72,8 +72,10 @@ def test_int_shard_edge_cases():
         assert _shards_int("glynn", rect, world, "int128") == ref
         assert _shards_int("ryser", rect, world, "int128") == ref
         assert _shards_int("glynn", rect, world, None) == ref
-    with pytest.raises(ValueError):  # checked rect Ryser follows the combination order: not sharded
+    with pytest.raises(ValueError):  # checked rect Ryser follows the combination order: no Gray shards
         _shards_int("ryser", rect, 2, None)
+    # ... so sharded_permanent evaluates it whole on every rank (world of one here)
+    assert P.sharded_permanent(rect, alg="ryser") == ref
     with pytest.raises(ValueError):  # partial of the other width
         p = S.gpu_partial_int("glynn", rect, 0, 1 << 12, exact=None)
         S.finish_int("glynn", rect, p[None, :], exact="int128")

@@ -207,3 +207,31 @@ class TestContracts:
     def test_exact_mode_validated(self):
         with pytest.raises(ValueError):
             permanent_glynn_square(as_matrix(np.eye(2, dtype=np.int64)), exact="int256")
+
+
+def test_opt_selection_policy(monkeypatch):
+    """permanent_opt's choice without a GPU (run_algorithm stubbed):
+    integer matrices use the reference's table (same checked
+    algorithm => same OverflowError), floats the B200 table, and past the
+    fitted grid (n > 34) a 16x cheaper algorithm overrides the table."""
+    from paper_2510_03421_b200 import dispatch as D
+
+    picked = []
+    monkeypatch.setattr(D, "run_algorithm", lambda mat, alg, **kw: picked.append(alg))
+    monkeypatch.delenv("PERMANENT_TUNING_FILE", raising=False)
+    for m, n in ((6, 6), (5, 5), (3, 9), (12, 12), (20, 20)):
+        picked.clear()
+        D.permanent_opt(np.ones((m, n), dtype=np.int64))
+        assert picked == [D.select_algorithm(m, n, D.default_params())]
+        picked.clear()
+        D.permanent_opt(np.ones((m, n)))
+        assert picked == [D.select_algorithm(m, n, D.b200_params())]
+    for (m, n), want in (((8, 62), D.AlgorithmId.RYSER), ((2, 70), D.AlgorithmId.COMBINATORIC),
+                         ((36, 36), D.AlgorithmId.GLYNN), ((30, 40), D.AlgorithmId.GLYNN)):
+        picked.clear()
+        D.permanent_opt(np.ones((m, n)))
+        assert picked == [want], (m, n)
+        assert D.engine_choice(m, n, D.b200_params()) is want
+    picked.clear()
+    D.permanent_opt(np.ones((8, 62)), params=D.b200_params())  # explicit params: the pure rule
+    assert picked == [D.select_algorithm(8, 62, D.b200_params())]

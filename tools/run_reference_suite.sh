@@ -5,7 +5,7 @@
 #   bash tools/run_reference_suite.sh OUT.txt [pytest args]
 set -u
 ROOT="$(cd "$(dirname "$0")/.." && pwd)"
-OUT="${1:-$ROOT/gpurun_out/refsuite.txt}"
+OUT="$(realpath -m "${1:-$ROOT/gpurun_out/refsuite.txt}")"
 if [ ! -d "$ROOT/scratch_reftests" ]; then
   if [ -d /root/reference/pkg/tests ]; then
     cp -r /root/reference/pkg/tests "$ROOT/scratch_reftests"
