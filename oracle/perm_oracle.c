@@ -30,6 +30,11 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* Column limit of the permutation / combination forms: the reference caps
+ * only its Gray walks at 62 columns (src/algorithms.py:47), so the DFS and
+ * the combination-order Ryser take any width up to this bound. */
+#define ORC_MAX_COLS 256
+
 typedef struct { double re, im; } cplx;
 typedef __int128 i128;
 typedef unsigned __int128 u128;
@@ -56,7 +61,7 @@ double orc_comb_f64(int m, int n, const double* a) {
   double zero = a[0] - a[0];
   int64_t choice[64];
   double prod[65];
-  unsigned char used[64];
+  unsigned char used[ORC_MAX_COLS];
   for (int i = 0; i < m; ++i) choice[i] = -1;
   memset(used, 0, sizeof used);
   prod[0] = zero + 1.0;
@@ -86,7 +91,7 @@ void orc_comb_c128(int m, int n, const double* a_, double* out) {
   cplx zero = c_sub(a[0], a[0]);
   int64_t choice[64];
   cplx prod[65];
-  unsigned char used[64];
+  unsigned char used[ORC_MAX_COLS];
   for (int i = 0; i < m; ++i) choice[i] = -1;
   memset(used, 0, sizeof used);
   prod[0] = zero; prod[0].re = zero.re + 1.0; prod[0].im = zero.im + 0.0;
@@ -122,7 +127,7 @@ void orc_comb_c128(int m, int n, const double* a_, double* out) {
 int orc_comb_i64(int m, int n, const int64_t* a, int64_t* out) {
   int64_t choice[64];
   int64_t prod[65];
-  unsigned char used[64];
+  unsigned char used[ORC_MAX_COLS];
   for (int i = 0; i < m; ++i) choice[i] = -1;
   memset(used, 0, sizeof used);
   prod[0] = 1;
@@ -232,12 +237,16 @@ int orc_ryser_sq_i64(int n, const int64_t* a, int64_t* out) {
   return 0;
 }
 
-/* Binomial C(a, b) exactly (a <= 62). */
+/* Binomial C(a, b) exactly, or -1 when it exceeds int64 (the running
+ * product C(a-b+i, i) stays exact: each step is an exact division). */
 static int64_t binom_i64(int a, int b) {
   if (b < 0 || b > a) return 0;
   u128 r = 1;
-  for (int i = 1; i <= b; ++i) r = r * (u128)(a - b + i) / (u128)i;
-  return (int64_t)r;
+  for (int i = 1; i <= b; ++i) {
+    if (r > ((u128)1 << 120) / (u128)(a - b + i)) return -1;
+    r = r * (u128)(a - b + i) / (u128)i;
+  }
+  return r > (u128)INT64_MAX ? -1 : (int64_t)r;
 }
 
 /* _ryser_weights (src/algorithms.py:110-115) converted to float64 the way
@@ -330,12 +339,13 @@ void orc_ryser_rect_c128(int m, int n, const double* a_, double* out) {
   out[0] = total.re; out[1] = total.im;
 }
 
-/* ryser_rect_int: src/_kernels.py:265-365 (weights always fit int64 for
- * n <= 62, so the src/algorithms.py:129-130 guard never fires). */
+/* ryser_rect_int: src/_kernels.py:265-365; a weight above int64 is the
+ * src/algorithms.py:129-130 overflow. */
 int orc_ryser_rect_i64(int m, int n, const int64_t* a, int64_t* out) {
   int64_t w[65];
   for (int s = 1; s <= m; ++s) {
     int64_t c = binom_i64(n - s, m - s);
+    if (c < 0) { *out = 0; return 1; }
     w[s] = ((m - s) & 1) ? -c : c;
   }
   int64_t comb[64];

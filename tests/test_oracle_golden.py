@@ -133,3 +133,15 @@ def test_magnitude_sum_two_restatements_agree(rng):
         _, _, mg = O.walk_dd_mt(O.walk_setup("glynn", a, scale=sc), nthreads=2, mag=True)
         viac = mg / (2.0 ** (n - 1) * math.factorial(n - m) * sc ** m)
         assert abs(brute - viac) <= 1e-13 * brute, (m, n, cplx, brute, viac)
+
+
+def test_wide_column_forms(rng):
+    """Past 62 columns (no cap in the reference's combinatoric / ryser_rect):
+    the oracle's DFS and combination-order Ryser agree with brute force."""
+    for m, n in ((1, 200), (2, 90), (3, 70)):
+        a = rng.integers(-3, 4, (m, n)).astype(np.int64)
+        exact = O.brute_force(a.tolist())
+        assert O.permanent("combinatoric", a) == (exact, False)
+        assert O.kernel("ryser_rect", a) == (exact, False)
+        f = a.astype(np.float64)
+        assert O.permanent("combinatoric", f)[0] == exact
