@@ -28,7 +28,11 @@ int tiny_permanent(int alg, bool cplx, int m, int n, const double* a, double* ou
 static int tiny_glynn_max_n() {
   static const int v = [] {
     const char* e = std::getenv("PERM_TINY_GLYNN_MAX_N");
-    return (e && *e) ? std::atoi(e) : 12;
+    // 0 (off): since the walk path went zero-copy (setup as kernel
+    // parameters, mapped result; one warp below 256 steps) it beats the
+    // warp-per-matrix batch kernel at every n (profiles/r2_tiny_glynn_threshold.txt,
+    // r2_dispatch_fit.txt); PERM_TINY_GLYNN_MAX_N=12 restores the old route
+    return (e && *e) ? std::atoi(e) : 0;
   }();
   return v;
 }
@@ -61,18 +65,29 @@ int check_shape(int alg, int m, int n) {
   return PERM_OK;
 }
 
-// Rectangular Ryser: the all-subsets Gray walk costs 2^n steps, the
-// reference's combination order sum_{s<=m} C(n,s); the latter wins for very
-// rectangular shapes despite its heavier per-step update.
+// Rectangular Ryser: the all-subsets weighted Gray walk (2^n steps) or the
+// reference's combination order (sum_{s<=m} C(n, s) subsets), whichever the
+// B200 cost model measured faster (tools/ryser_rect_probe.py,
+// profiles/r2_ryser_rect.txt; per-call microseconds through the public API):
+//   walk ~ 27 + 2^n (0.4 + 0.11 m) 1e-3   (zero-copy walk: latency floor 27 us)
+//   comb ~ 36 + C (10 + 12 m) 1e-3        (combination kernels: floor 36 us)
 bool ryser_rect_use_comb(int m, int n) {
   if (m >= n) return false;
   if (n > 62) return true;
+  static const int force = [] {  // PERM_RYSER_RECT = "walk" / "comb" (experiments)
+    const char* e = std::getenv("PERM_RYSER_RECT");
+    if (!e || !*e) return 0;
+    return std::string(e) == "comb" ? 1 : std::string(e) == "walk" ? 2 : 0;
+  }();
+  if (force) return force == 1;
   long double c = 0, b = 1;  // running C(n, s)
   for (int s = 1; s <= m; ++s) {
     b = b * (n - s + 1) / s;
     c += b;
   }
-  return c * 8.0L < std::ldexp(1.0L, n);
+  const long double walk_us = 27.0L + std::ldexp(1.0L, n) * (0.4L + 0.11L * m) * 1e-3L;
+  const long double comb_us = 36.0L + c * (10.0L + 12.0L * m) * 1e-3L;
+  return comb_us < walk_us;
 }
 
 // Single permanent through the walk engine; returns normalized value.
@@ -85,15 +100,12 @@ int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, 
     return comb_permanent(true, cplx ? 1 : 0, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream_);
   int st = check_shape(alg, m, n);
   if (st) return st;
-  // walks shorter than one warp-group of chunks (Glynn n <= 8, Ryser n <= 7):
-  // the register-resident thread-per-matrix batch kernels, batch of one
-  if (magsum == nullptr && !dev_ptr && lda == n && walk_steps(alg, m, n) < 256) {
-    if (stream_ == nullptr) {  // zero-copy round trip (mapped pinned memory, flag spin)
-      const int tst = tiny_permanent(alg, cplx, m, n, a, out);
-      if (tst >= 0) return tst;
-    }
+  // walks shorter than one warp-group of chunks (Glynn n <= 8, Ryser n <= 7)
+  // on a caller's stream: the register-resident thread-per-matrix batch
+  // kernels, batch of one (the default stream takes the zero-copy one-warp
+  // walk below, which measured faster: profiles/r2_dispatch_fit.txt)
+  if (magsum == nullptr && !dev_ptr && lda == n && walk_steps(alg, m, n) < 256 && stream_ != nullptr)
     return batch_permanent(alg, cplx, 1, m, n, a, out, 0, stream_);
-  }
   // Glynn n = 9..TINY_GLYNN_MAX_N (rectangles ones-padded and pre-scaled on the
   // host): one warp walks the matrix (the
   // warp-per-matrix batch kernel) on the zero-copy path, cheaper than a
@@ -110,19 +122,12 @@ int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, 
   WalkSetup ws;
   st = build_walk(alg, A, &ws, /*exact_state=*/true);
   if (st) return st;
-  Scratch* s = scratch();
-  if (!s) return cuda_fail(cudaErrorNoDevice, "scratch");
-  // result slot: reserve 8 doubles after the walk data in scratch
-  const size_t part_bytes = (size_t)kMaxPartials * kPartialStride * sizeof(double);
-  const size_t need = part_bytes + ws.buf.size() * sizeof(double) + 64 * sizeof(double);
-  st = ensure_dev(s, need + 256);
+  // default stream: the zero-copy path (setup as kernel parameters, result
+  // through mapped memory); a caller's stream keeps stream-ordered copies
+  double r8[8];
+  st = run_walk_host(ws, 0, walk_steps(alg, m, n), magsum != nullptr, r8, stream, stream_ == nullptr);
   if (st) return st;
-  double* dst = reinterpret_cast<double*>(static_cast<char*>(s->dev) + s->dev_cap) - 8;
-  st = run_walk(ws, 0, walk_steps(alg, m, n), magsum != nullptr, dst, stream);
-  if (st) return st;
-  PERM_CUDA_TRY(cudaMemcpyAsync(s->host, dst, 8 * sizeof(double), cudaMemcpyDeviceToHost, stream));
-  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
-  double re = s->host[0] + s->host[1], im = s->host[2] + s->host[3], mg = s->host[4];
+  double re = r8[0] + r8[1], im = r8[2] + r8[3], mg = r8[4];
   normalize(alg, m, n, ws.scale_log2, &re, &im, &mg);
   out[0] = re;
   if (cplx) out[1] = im;
@@ -160,16 +165,10 @@ int walk_partial(int alg, bool cplx, int m, int n, const double* a, int64_t lda,
     }
     return PERM_OK;
   }
-  double* dst = partial_on_device ? partial
-                                  : reinterpret_cast<double*>(static_cast<char*>(s->dev) + s->dev_cap) - 8;
-  st = run_walk(ws, k_begin, k_end, mag, dst, stream);
+  if (!partial_on_device) return run_walk_host(ws, k_begin, k_end, mag, partial, stream, stream_ == nullptr);
+  st = run_walk(ws, k_begin, k_end, mag, partial, stream);
   if (st) return st;
-  if (partial_on_device) s->async_pending = true;
-  if (!partial_on_device) {
-    PERM_CUDA_TRY(cudaMemcpyAsync(s->host, dst, 8 * sizeof(double), cudaMemcpyDeviceToHost, stream));
-    PERM_CUDA_TRY(cudaStreamSynchronize(stream));
-    std::copy(s->host, s->host + 8, partial);
-  }
+  s->async_pending = true;
   return PERM_OK;
 }
 

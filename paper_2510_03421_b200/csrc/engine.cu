@@ -2,6 +2,7 @@
 // setup/normalization and the fixed-order finalize kernel.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 
 #include "engine.cuh"
@@ -158,6 +159,19 @@ static inline double binom_d(int a, int b) {
 // of the unquantized walk at 30-100x the error this leaves.  Real and
 // imaginary parts get their own grids.  Integer-valued matrices are already
 // on every grid q <= 1 and stay bit-identical.
+// x rounded to the nearest multiple of 2^qe (ties to even).  |x| < 2^(qe+51):
+// one add and one subtract of C = 1.5 * 2^(qe+52), whose binade has ulp
+// 2^qe (the walk's setup is on the per-call path: libm ldexp / nearbyint per
+// entry cost ~6 us at n = 20); larger |x| (one entry carrying most of its
+// line) and grids near the top of the range take the exact libm path.
+static inline double round_to_grid(double x, int qe, double C, bool magic_ok) {
+  if (magic_ok && std::fabs(x) < C * (1.0 / 3.0)) {
+    const double t = x + C;  // IEEE semantics (no -ffast-math): not folded
+    return t - C;
+  }
+  return std::ldexp(std::nearbyint(std::ldexp(x, -qe)), qe);
+}
+
 static void quantize_line(double* x, size_t count, size_t stride, const std::vector<size_t>& keep_exact) {
   long double c = 0;
   for (size_t k = 0; k < count; ++k) c += std::fabs((long double)x[k * stride]);
@@ -165,23 +179,27 @@ static void quantize_line(double* x, size_t count, size_t stride, const std::vec
   int e = 0;
   std::frexp((double)c * (1.0 + 4e-16), &e);  // c <= 2^e (margin for the long double -> double cast)
   const int qe = std::max(e - 52, -1074);
+  const bool magic_ok = qe + 52 <= 1000;
+  const double C = magic_ok ? std::ldexp(1.5, qe + 52) : 0.0;
   for (size_t k : keep_exact) {  // ones rows of rectangular Glynn must stay on the grid
-    const double r = std::ldexp(std::nearbyint(std::ldexp(x[k * stride], -qe)), qe);
-    if (r != x[k * stride]) return;
+    if (round_to_grid(x[k * stride], qe, C, magic_ok) != x[k * stride]) return;
   }
-  for (size_t k = 0; k < count; ++k) x[k * stride] = std::ldexp(std::nearbyint(std::ldexp(x[k * stride], -qe)), qe);
+  for (size_t k = 0; k < count; ++k) x[k * stride] = round_to_grid(x[k * stride], qe, C, magic_ok);
 }
 
 int build_walk(int alg, const HostMat& A, WalkSetup* ws, bool exact_state) {
   const int m = A.m, n = A.n;
   const int w = A.cplx ? 2 : 1;
   ws->cplx = A.cplx;
+  ws->exact = exact_state;
   ws->scale_log2 = 0;
   ws->weighted = false;
   ws->wlen = 0;
   if (alg == PERM_ALG_GLYNN) {
     // ones-padded n x n matrix, real rows scaled by k = 2^s
     const int s = (m < n) ? prescale_log2(A) : 0;
+    const bool fast_scale = std::abs(s) <= 1000;  // x * 2^s == ldexp(x, s) while 2^s is finite
+    const double ks = fast_scale ? std::ldexp(1.0, s) : 1.0;
     ws->scale_log2 = s;
     ws->P = n;
     ws->B = n - 1;
@@ -192,8 +210,9 @@ int build_walk(int alg, const HostMat& A, WalkSetup* ws, bool exact_state) {
     std::vector<double> G((size_t)n * n * w);
     for (int i = 0; i < n; ++i)
       for (int j = 0; j < n; ++j) {
-        G[((size_t)i * n + j) * w] = i < m ? std::ldexp(A.re(i, j), s) : 1.0;
-        if (w == 2) G[((size_t)i * n + j) * w + 1] = i < m ? std::ldexp(A.im(i, j), s) : 0.0;
+        G[((size_t)i * n + j) * w] = i < m ? (fast_scale ? A.re(i, j) * ks : std::ldexp(A.re(i, j), s)) : 1.0;
+        if (w == 2)
+          G[((size_t)i * n + j) * w + 1] = i < m ? (fast_scale ? A.im(i, j) * ks : std::ldexp(A.im(i, j), s)) : 0.0;
       }
     if (exact_state) {
       std::vector<size_t> ones;
@@ -364,7 +383,14 @@ walk_fn walk_lookup(int dtype, bool weighted, int P) {
   return weighted ? walk_lookup_c128_w1(P) : walk_lookup_c128_w0(P);
 }
 
-int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst, cudaStream_t stream) {
+static bool walk_inline_fits(const WalkSetup& ws) {
+  if (ws.weighted ? (ws.B > 62 || ws.wlen > 63) : ws.B > ws.P) return false;
+  const size_t bytes = (size_t)walk_inline_doubles(ws.P, ws.cplx ? 2 : 1, ws.weighted) * sizeof(double);
+  return bytes <= kWalkInlineMaxBytes;
+}
+
+static int launch_setup(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst,
+                        unsigned int* flag, unsigned int seq, bool allow_inline, cudaStream_t stream) {
   if (ws.P < 1 || ws.P > 64) {
     set_error("state length out of range (1..64)");
     return PERM_BAD_SHAPE;
@@ -380,8 +406,12 @@ int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, dou
   if (st) return st;
   double* partials = static_cast<double*>(s->dev);
   double* data = partials + (size_t)kMaxPartials * kPartialStride;
-  st = stage_h2d(s, data, ws.buf.data(), data_bytes, stream);
-  if (st) return st;
+  const uint64_t steps = k_end - k_begin;
+  const bool inl = allow_inline && (walk_tiled(k_begin, steps) || (steps > 0 && steps < 256)) && walk_inline_fits(ws);
+  if (!inl) {
+    st = stage_h2d(s, data, ws.buf.data(), data_bytes, stream);
+    if (st) return st;
+  }
   walk_fn fn = walk_lookup(ws.cplx ? 1 : 0, ws.weighted, ws.P);
   if (!fn) {
     set_error("no walk kernel for this state length");
@@ -402,6 +432,9 @@ int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, dou
   job.partials = partials;
   job.final_out = dst;
   job.done = s->done;
+  job.inline_host = inl ? ws.buf.data() : nullptr;
+  job.flag = flag;
+  job.seq = seq;
   WalkPlan plan;
   KernelTimer& tm = kernel_timer();
   const bool timed = tm.ok && timing_enabled();
@@ -411,6 +444,66 @@ int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, dou
   tm.pending = timed;
   tm.last_grid = plan.grid;
   tm.last_log2L = plan.log2L;
+  return PERM_OK;
+}
+
+int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst, cudaStream_t stream) {
+  return launch_setup(ws, k_begin, k_end, mag, dst, nullptr, 0, true, stream);
+}
+
+static int mapped_slot(Scratch* s) {
+  if (s->mres_host) return PERM_OK;
+  PERM_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&s->mres_host), 8 * sizeof(double) + 64, cudaHostAllocMapped));
+  PERM_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->mres_dev), s->mres_host, 0));
+  s->mflag_host = reinterpret_cast<unsigned int*>(s->mres_host + 8);
+  s->mflag_dev = reinterpret_cast<unsigned int*>(s->mres_dev + 8);
+  *reinterpret_cast<volatile unsigned int*>(s->mflag_host) = 0;
+  return PERM_OK;
+}
+
+int run_walk_host(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* host8,
+                  cudaStream_t stream, bool zero_copy) {
+  Scratch* s = scratch();
+  if (!s) return cuda_fail(cudaErrorNoDevice, "scratch");
+  const uint64_t steps = k_end - k_begin;
+  if (zero_copy && (walk_tiled(k_begin, steps) || (steps > 0 && steps < 256)) && walk_inline_fits(ws)) {
+    int st = mapped_slot(s);
+    if (st) return st;
+    if (s->async_pending) {  // an earlier device-output call may still use the scratch
+      PERM_CUDA_TRY(cudaDeviceSynchronize());
+      s->async_pending = false;
+    }
+    const unsigned int seq = ++s->mseq;
+    st = launch_setup(ws, k_begin, k_end, mag, s->mres_dev, s->mflag_dev, seq, true, stream);
+    if (st) return st;
+    // spin on the flag; after 2 ms fall back to a blocking wait (which also
+    // surfaces launch / execution errors)
+    volatile unsigned int* f = s->mflag_host;
+    const auto t0 = std::chrono::steady_clock::now();
+    while (*f != seq) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) {
+        PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+        if (*f != seq) {
+          set_error("walk finished without publishing its result");
+          return PERM_CUDA;
+        }
+        break;
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const volatile double* r = s->mres_host;
+    for (int i = 0; i < 8; ++i) host8[i] = r[i];
+    return PERM_OK;
+  }
+  const size_t part_bytes = (size_t)kMaxPartials * kPartialStride * sizeof(double);
+  int st = ensure_dev(s, part_bytes + ws.buf.size() * sizeof(double) + 64 * sizeof(double) + 256);
+  if (st) return st;
+  double* dst = reinterpret_cast<double*>(static_cast<char*>(s->dev) + s->dev_cap) - 8;
+  st = run_walk(ws, k_begin, k_end, mag, dst, stream);
+  if (st) return st;
+  PERM_CUDA_TRY(cudaMemcpyAsync(s->host, dst, 8 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  std::copy(s->host, s->host + 8, host8);
   return PERM_OK;
 }
 

@@ -36,6 +36,13 @@ struct Scratch {
   unsigned int* done = nullptr;  // walk kernels' last-block counter (device)
   bool async_pending = false;    // a device-output call may still be running
   cudaStream_t own = nullptr;
+  // mapped pinned result slot of the zero-copy single-walk path: the walk's
+  // last block writes 8 doubles here and then flag = seq (walk.cuh)
+  double* mres_host = nullptr;
+  double* mres_dev = nullptr;
+  unsigned int* mflag_host = nullptr;
+  unsigned int* mflag_dev = nullptr;
+  unsigned int mseq = 0;
 };
 constexpr size_t kHostResultDoubles = 16384;    // pinned result buffer size
 Scratch* scratch();                              // for the current device
@@ -65,6 +72,7 @@ struct WalkSetup {
   std::vector<double> buf;           // v0 [P], U [B][P] (complex interleaved), then w [n+1]
   size_t v0_off = 0, U_off = 0, w_off = 0;  // offsets in doubles
   int wlen = 0;
+  bool exact = false;                // state lines on the exact grid (no re-seeding needed)
 };
 // exact_state: round each state line (Glynn column / Ryser row) to a grid on
 // which every walk state is exact (the float walks; not the double-double
@@ -76,6 +84,11 @@ int prescale_log2(const HostMat& A);
 void normalize(int alg, int m, int n, int scale_log2, double* re, double* im, double* mag);
 // Run the walk over [k_begin, k_end) -> 8 raw doubles at `dst` (device).
 int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst, cudaStream_t stream);
+// Whole walk with the 8 raw result doubles returned in host memory: the
+// zero-copy path (setup as kernel parameters, result + flag in mapped pinned
+// memory, spin on the flag) where it applies, else run_walk + copy + sync.
+int run_walk_host(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* host8,
+                  cudaStream_t stream, bool zero_copy);
 
 uint64_t walk_steps(int alg, int m, int n);
 

@@ -52,15 +52,21 @@ struct WalkArgs {
   uint64_t k_begin;      // first Gray index, multiple of 32*L
   uint64_t ngroups;      // number of 32-chunk groups
   double* partials;      // [gridDim.x][kPartialStride]
-  double* final_out;     // 8 doubles: fixed-order sum of all block partials
+  double* final_out;     // 8 doubles: fixed-order sum of all block partials (device or mapped host)
   unsigned int* done;    // block-completion counter (0 on entry, reset on exit)
+  unsigned int* flag;    // optional mapped host flag, set to seq once final_out is written
+  unsigned int seq;
 };
 
 // Last-block-done combine: every block publishes its partial, the block that
 // arrives last sums all partials in block order (deterministic for a given
 // grid) and writes the final 8 doubles -- no separate finalize launch.
+// `flag` (optional, mapped host memory): after final_out -- then also host
+// memory -- is written, a system-scope fence and flag = seq, so the caller
+// can spin on the flag instead of a device-to-host copy and a stream sync.
 __device__ __forceinline__ void walk_last_block_combine(const double* partials, double* final_out,
-                                                        unsigned int* done) {
+                                                        unsigned int* done, unsigned int* flag = nullptr,
+                                                        unsigned int seq = 0) {
   __shared__ bool last;
   if (threadIdx.x == 0) {
     __threadfence();
@@ -98,6 +104,14 @@ __device__ __forceinline__ void walk_last_block_combine(const double* partials, 
     final_out[0] = H; final_out[1] = Lo; final_out[2] = H2; final_out[3] = L2; final_out[4] = M;
     final_out[5] = 0.0; final_out[6] = 0.0; final_out[7] = 0.0;
     *done = 0u;  // ready for the next launch on this scratch
+    if (flag) {  // release at system scope: final_out (this thread's stores) first
+#ifdef WALK_FLAG_FENCE
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned int*>(flag) = seq;
+#else
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
+#endif
+    }
   }
 }
 
@@ -582,19 +596,96 @@ __device__ __forceinline__ void walk_block_reduce(WalkAcc A, double* out) {
     red[warp][0] = A.hi; red[warp][1] = A.lo; red[warp][2] = A.hi_i; red[warp][3] = A.lo_i; red[warp][4] = A.mag;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double H = red[0][0], Lo = red[0][1], Hi2 = red[0][2], Lo2 = red[0][3], M = red[0][4];
-    for (int w = 1; w < kWalkWarps; ++w) {
-      dd_add(H, Lo, red[w][0], red[w][1]);
-      dd_add(Hi2, Lo2, red[w][2], red[w][3]);
-      M += red[w][4];
+  // warp leaders combined by warp 0 with a 3-level shuffle tree (a serial
+  // loop on one thread was ~0.3 us of dependent double-double adds)
+  if (warp == 0) {
+    double H = 0.0, Lo = 0.0, H2 = 0.0, L2 = 0.0, M = 0.0;
+    if (lane < kWalkWarps) {
+      H = red[lane][0]; Lo = red[lane][1]; H2 = red[lane][2]; L2 = red[lane][3]; M = red[lane][4];
     }
-    out[0] = H; out[1] = Lo; out[2] = Hi2; out[3] = Lo2; out[4] = M;
+#pragma unroll
+    for (int off = kWalkWarps / 2; off > 0; off >>= 1) {
+      double h = __shfl_down_sync(0xffffffffu, H, off), l = __shfl_down_sync(0xffffffffu, Lo, off);
+      dd_add(H, Lo, h, l);
+      if constexpr (CPLX) {
+        double h3 = __shfl_down_sync(0xffffffffu, H2, off), l3 = __shfl_down_sync(0xffffffffu, L2, off);
+        dd_add(H2, L2, h3, l3);
+      }
+      M += __shfl_down_sync(0xffffffffu, M, off);
+    }
+    if (lane == 0) {
+      out[0] = H; out[1] = Lo; out[2] = H2; out[3] = L2; out[4] = M;
+    }
   }
 }
 
+// Setup passed by value in the launch (kernel parameters, <= 32 KB) for the
+// small walks, where a staged host-to-device copy costs as much as the walk:
+// [v0 (P) | U (B x P)], B <= P, unpadded (WalkSetup::buf's layout).
+// Doubles of the inline blob: [v0 | U | w] with B <= P rows (unweighted) or
+// B <= 62 rows and <= 63 popcount weights (weighted rectangular Ryser).
+__host__ __device__ constexpr int walk_inline_doubles(int P, int kD, bool W) {
+  return W ? 63 * P * kD + 64 : (P + 1) * P * kD;
+}
 template <typename T, int P, bool W>
-__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_kernel(WalkArgs args) {
+struct WalkInline {
+  alignas(16) double d[walk_inline_doubles(P, Num<T>::kDoubles, W)];
+};
+// The kernel's second parameter: the inline setup, or nothing.  (WalkArgs
+// stays a separate by-value parameter: folded into one __grid_constant__
+// struct its fields were read per thread, and the chunk loop's bookkeeping
+// left the uniform datapath -- 6% slower at n = 32..36.)
+template <typename T, int P, bool W, bool INL>
+struct WalkBlob {
+  int unused;
+};
+template <typename T, int P, bool W>
+struct WalkBlob<T, P, W, true> : WalkInline<T, P, W> {};
+
+// Timeline probe (tools/small_walk_exp.cu builds with -DWALK_TIMELINE):
+// %globaltimer of thread 0 of every block at each phase boundary.
+#ifdef WALK_TIMELINE
+__device__ unsigned long long* g_walk_tl;
+#define WALK_TL(i)                                                  \
+  do {                                                               \
+    if (threadIdx.x == 0 && g_walk_tl) {                             \
+      unsigned long long t_;                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));         \
+      g_walk_tl[blockIdx.x * 8 + (i)] = t_;                          \
+    }                                                                \
+  } while (0)
+#else
+#define WALK_TL(i) \
+  do {             \
+  } while (0)
+#endif
+
+// Stage [v0 | U] (contiguous, inline or in device memory) into shared memory
+// in batches of 4 independent loads per thread before their stores: one load
+// latency per batch instead of one per element (a plain loop serialized them).
+template <typename T, int P>
+__device__ __forceinline__ void walk_stage(const T* __restrict__ src, int B, T* sU, T* sV0) {
+  constexpr int PS = row_stride<T, P>();
+  const int total = (B + 1) * P;
+  for (int base = 0; base < total; base += 4 * kWalkThreads) {
+    T r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = base + k * kWalkThreads + (int)threadIdx.x;
+      if (e < total) r[k] = src[e];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = base + k * kWalkThreads + (int)threadIdx.x;
+      if (e < P) sV0[e] = r[k];
+      else if (e < total) sU[(e / P - 1) * PS + (e % P)] = r[k];
+    }
+  }
+}
+
+template <typename T, int P, bool W, bool INL>
+__global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>())
+    walk_kernel(WalkArgs args, const __grid_constant__ WalkBlob<T, P, W, INL> blob) {
   constexpr int PS = row_stride<T, P>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sU = reinterpret_cast<T*>(smem_raw);        // [B][PS]
@@ -605,13 +696,13 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_ke
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int B = args.B;
-  {
-    const T* gU = static_cast<const T*>(args.U);
-    const T* gV0 = static_cast<const T*>(args.v0);
-    for (int i = tid; i < B * P; i += kWalkThreads) sU[(i / P) * PS + (i % P)] = gU[i];
-    for (int j = tid; j < P; j += kWalkThreads) sV0[j] = gV0[j];
-    if constexpr (W)
-      for (int i = tid; i < args.wlen; i += kWalkThreads) sW[i] = args.w[i];
+  WALK_TL(0);
+  if constexpr (INL) walk_stage<T, P>(reinterpret_cast<const T*>(blob.d), B, sU, sV0);
+  else walk_stage<T, P>(static_cast<const T*>(args.v0), B, sU, sV0);
+  if constexpr (W) {
+    const double* w = args.w;
+    if constexpr (INL) w = blob.d + (size_t)(B + 1) * P * Num<T>::kDoubles;
+    for (int i = tid; i < args.wlen; i += kWalkThreads) sW[i] = w[i];
   }
   __syncthreads();
 
@@ -620,12 +711,16 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_ke
 #pragma unroll
     for (int j = 0; j < P; ++j) u0[j] = sU[j];
   }
+  WALK_TL(1);
   WalkAcc A;
   walk_group_range<T, P, W>(sU, sV0, sWarp + warp * PS, sW, u0, B, args.log2L, args.k_begin,
                             (uint64_t)blockIdx.x * kWalkWarps + warp, args.ngroups,
                             (uint64_t)gridDim.x * kWalkWarps, args.mag, A);
+  WALK_TL(2);
   walk_block_reduce<sizeof(T) == 16>(A, args.partials + (size_t)blockIdx.x * kPartialStride);
-  walk_last_block_combine(args.partials, args.final_out, args.done);
+  WALK_TL(3);
+  walk_last_block_combine(args.partials, args.final_out, args.done, args.flag, args.seq);
+  WALK_TL(4);
 }
 
 // Many square Glynn permanents in one launch (batches of n = 17..30): work
@@ -744,6 +839,63 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_mu
       static_cast<T*>(args.out)[mat] = r;
       args.done[mat] = 0u;
     }
+  }
+}
+
+// One warp over a short range (< 256 steps: Glynn n <= 8, Ryser n <= 7) with
+// the setup as kernel parameters and the result published through mapped
+// memory (final_out, flag): the zero-copy single-permanent path below the
+// chunked kernel's minimum.  Lane l walks [k_begin + l s / 32, ...) from its
+// own seed (v0 + the rows of its Gray code), fixed-order warp reduction.
+template <typename T, int P, bool W>
+__global__ void __launch_bounds__(32) walk_tiny_kernel(WalkArgs args, const __grid_constant__ WalkBlob<T, P, W, true> blob,
+                                                       uint64_t k_end) {
+  const int lane = threadIdx.x;
+  const T* v0 = reinterpret_cast<const T*>(blob.d);
+  const T* U = v0 + P;
+  const double* w = blob.d + (size_t)(args.B + 1) * P * Num<T>::kDoubles;
+  const uint64_t steps = k_end - args.k_begin;
+  const uint64_t k0 = args.k_begin + steps * lane / 32, k1 = args.k_begin + steps * (lane + 1) / 32;
+  T v[P];
+  const uint64_t g0 = k0 ^ (k0 >> 1);
+#pragma unroll
+  for (int j = 0; j < P; ++j) v[j] = v0[j];
+  for (int t = 0; t < args.B; ++t)
+    if ((g0 >> t) & 1) {
+#pragma unroll
+      for (int j = 0; j < P; ++j) v[j] = Num<T>::add(v[j], U[t * P + j]);
+    }
+  int pc = __popcll(g0);
+  T acc = Num<T>::zero();
+  double mag = 0.0;
+  for (uint64_t k = k0; k < k1; ++k) {
+    if (k != k0) {
+      const int t = __ffsll((long long)k) - 1;
+      const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
+#pragma unroll
+      for (int j = 0; j < P; ++j) v[j] = set ? Num<T>::add(v[j], U[t * P + j]) : Num<T>::sub(v[j], U[t * P + j]);
+      pc += set ? 1 : -1;
+    }
+    const T p = tree_product<T, P>(v);
+    if constexpr (W) {
+      acc = Num<T>::add(acc, Num<T>::scale(w[pc], p));
+      if (args.mag) mag += fabs(w[pc]) * Num<T>::absval(p);
+    } else {
+      acc = (k & 1) ? Num<T>::sub(acc, p) : Num<T>::add(acc, p);
+      if (args.mag) mag += Num<T>::absval(p);
+    }
+  }
+  double h = Num<T>::re(acc), l = 0.0, h2 = Num<T>::im(acc), l2 = 0.0;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    dd_add(h, l, __shfl_down_sync(0xffffffffu, h, off), __shfl_down_sync(0xffffffffu, l, off));
+    dd_add(h2, l2, __shfl_down_sync(0xffffffffu, h2, off), __shfl_down_sync(0xffffffffu, l2, off));
+    mag += __shfl_down_sync(0xffffffffu, mag, off);
+  }
+  if (lane == 0) {
+    double* o = args.final_out;
+    o[0] = h; o[1] = l; o[2] = h2; o[3] = l2; o[4] = mag; o[5] = 0.0; o[6] = 0.0; o[7] = 0.0;
+    if (args.flag) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(args.flag), "r"(args.seq) : "memory");
   }
 }
 

@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <utility>
 
 #include "walk.cuh"
@@ -24,7 +25,23 @@ struct WalkJob {
   double* partials;      // device scratch, >= max_partials() * kPartialStride doubles
   double* final_out;     // device, 8 doubles (combined result)
   unsigned int* done;    // device counter, zero on entry
+  // zero-copy launch: setup as kernel parameters, result + flag in mapped memory
+  const double* inline_host = nullptr;  // host copy of [v0 | U] to pass as kernel parameters
+  unsigned int* flag = nullptr;         // mapped host flag set to seq after final_out
+  unsigned int seq = 0;
 };
+
+// Inline setups (kernel parameters) up to this size: real P <= 26, complex
+// P <= 18.  A launch with 4-8 KB of parameters costs ~1-3 us more than an
+// empty one on B200 and the blocks read it at ~0.35 us/KB, which beats a
+// staged host-to-device copy (~5 us per call) while the walk is short; from
+// P = 28 the inline variant's walk measured 0.6-1.8% slower
+// (tools/small_walk_exp.cu, profiles/r2_small_walks.txt).
+constexpr size_t kWalkInlineMaxBytes = 5632;
+template <typename T, int P, bool W>
+__host__ __device__ constexpr bool walk_inline_ok() {
+  return sizeof(WalkInline<T, P, W>) <= kWalkInlineMaxBytes;
+}
 
 struct WalkPlan {
   int grid = 0;          // number of block partials written
@@ -82,12 +99,44 @@ inline int walk_max_log2L() {
 // Largest power-of-two alignment that divides x (x != 0), capped.
 inline int align_log2(uint64_t x) { return x ? __builtin_ctzll(x) : 64; }
 
-template <typename T, int P, bool W>
-cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream) {
+// Resident blocks per SM of `kern` with `smem` dynamic bytes, cached per
+// (kernel, smem, device): the query costs microseconds, comparable to a whole
+// n <= 22 walk.
+template <typename K>
+cudaError_t walk_occupancy(K kern, size_t smem, int* nsm_out, int* bps_out) {
+  // one slot per kernel (kernels of one signature share this instantiation)
+  static thread_local const void* cached_kern = nullptr;
+  static thread_local uint64_t cache = 0;  // smem << 32 | dev << 24 | bps << 12 | nsm; 0 = empty
+  int dev = 0, nsm = 148, bps = 1;
+  cudaGetDevice(&dev);
+  const uint64_t c = cached_kern == reinterpret_cast<const void*>(kern) ? cache : 0;
+  if (c && (c >> 32) == smem && (int)((c >> 24) & 0xff) == dev) {
+    bps = (int)((c >> 12) & 0xfff);
+    nsm = (int)(c & 0xfff);
+  } else {
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kWalkThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (bps < 1) bps = 1;
+    cache = ((uint64_t)smem << 32) | ((uint64_t)(dev & 0xff) << 24) | ((uint64_t)(bps & 0xfff) << 12) |
+            (uint64_t)(nsm & 0xfff);
+    cached_kern = reinterpret_cast<const void*>(kern);
+  }
+  *nsm_out = nsm;
+  *bps_out = bps;
+  return cudaSuccess;
+}
+
+// The chunked walk kernel applies when [k_begin, k_begin + steps) tiles into
+// groups of 32 chunks of >= 8 steps; other ranges run walk_small_kernel.
+inline bool walk_tiled(uint64_t k_begin, uint64_t steps) { return steps >= 256 && ((k_begin | steps) & 255) == 0; }
+
+template <typename T, int P, bool W, bool INL>
+cudaError_t launch_walk_impl(const WalkJob& job, WalkPlan* plan, cudaStream_t stream) {
   constexpr int PS = row_stride<T, P>();
   const uint64_t steps = job.k_end - job.k_begin;
   const size_t smem = (size_t)(job.B * PS + PS + kWalkWarps * PS) * sizeof(T) + (size_t)(W ? job.wlen : 0) * 8;
-  auto kern = walk_kernel<T, P, W>;
+  auto kern = walk_kernel<T, P, W, INL>;
   static int attr_smem = 0;  // benign race: idempotent
   if ((int)smem > 48 * 1024 && attr_smem < (int)smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -95,26 +144,8 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
     attr_smem = (int)smem;
   }
   int nsm = 148, bps = 1;
-  {
-    // occupancy depends only on (kernel, dynamic smem): cache the last answer
-    // (the query costs microseconds, comparable to a whole n <= 22 walk)
-    static std::atomic<uint64_t> cache{0};  // smem << 32 | dev << 24 | bps << 12 | nsm; 0 = empty
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t c = cache.load(std::memory_order_relaxed);
-    if (c && (c >> 32) == smem && (int)((c >> 24) & 0xff) == dev) {
-      bps = (int)((c >> 12) & 0xfff);
-      nsm = (int)(c & 0xfff);
-    } else {
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kWalkThreads, smem);
-      if (e != cudaSuccess) return e;
-      if (bps < 1) bps = 1;
-      cache.store(((uint64_t)smem << 32) | ((uint64_t)(dev & 0xff) << 24) | ((uint64_t)(bps & 0xfff) << 12) |
-                      (uint64_t)(nsm & 0xfff),
-                  std::memory_order_relaxed);
-    }
-  }
+  cudaError_t e = walk_occupancy(kern, smem, &nsm, &bps);
+  if (e != cudaSuccess) return e;
   if (bps * nsm > kMaxPartials) bps = kMaxPartials / nsm;
   const uint64_t lanes = (uint64_t)bps * nsm * kWalkThreads;
   // alignment: chunks of L must tile [k_begin, k_end) in groups of 32
@@ -122,6 +153,21 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
   const int amax = std::min(align_log2(job.k_begin), align_log2(steps)) - 5;
   if (r > amax) r = amax;
   if (r < 3 || (steps >> r) < 32) {
+    if constexpr (INL) {  // short range, setup inline: one warp (walk_tiny_kernel)
+      if (steps > 4096) return cudaErrorInvalidValue;
+      WalkBlob<T, P, W, true> blob{};
+      const size_t nd = (size_t)(P + (size_t)job.B * P) * Num<T>::kDoubles + (W ? (size_t)job.wlen : 0);
+      std::memcpy(blob.d, job.inline_host, nd * sizeof(double));
+      WalkArgs a{};
+      a.B = job.B; a.wlen = job.wlen; a.mag = job.mag; a.k_begin = job.k_begin;
+      a.final_out = job.final_out; a.flag = job.flag; a.seq = job.seq;
+      plan->small = true;
+      plan->grid = 1;
+      plan->log2L = 0;
+      walk_tiny_kernel<T, P, W><<<1, 32, 0, stream>>>(a, blob, job.k_end);
+      return cudaGetLastError();
+    }
+    if (job.flag) return cudaErrorInvalidValue;  // the flag path is inline-only
     plan->small = true;
     plan->grid = 1;
     plan->log2L = 0;
@@ -129,6 +175,8 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
                                                P, job.B, W ? 1 : 0, job.mag, job.k_begin, job.k_end, job.final_out);
     return cudaGetLastError();
   }
+  if (!INL && job.U != static_cast<const T*>(job.v0) + P) return cudaErrorInvalidValue;  // [v0 | U] contiguous
+  WalkBlob<T, P, W, INL> blob{};
   WalkArgs a;
   a.v0 = job.v0; a.U = job.U; a.w = job.w; a.B = job.B; a.log2L = r; a.wlen = job.wlen; a.mag = job.mag;
   a.k_begin = job.k_begin;
@@ -136,6 +184,12 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
   a.partials = job.partials;
   a.final_out = job.final_out;
   a.done = job.done;
+  a.flag = job.flag;
+  a.seq = job.seq;
+  if constexpr (INL) {
+    const size_t nd = (size_t)(P + (size_t)job.B * P) * Num<T>::kDoubles + (W ? (size_t)job.wlen : 0);
+    std::memcpy(blob.d, job.inline_host, nd * sizeof(double));
+  }
   uint64_t grid = (uint64_t)bps * nsm;
   const uint64_t need = (a.ngroups + kWalkWarps - 1) / kWalkWarps;
   if (grid > need) grid = need;
@@ -143,8 +197,20 @@ cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream)
   plan->grid = (int)grid;
   plan->log2L = r;
   plan->ngroups = a.ngroups;
-  kern<<<(unsigned)grid, kWalkThreads, smem, stream>>>(a);
+  kern<<<(unsigned)grid, kWalkThreads, smem, stream>>>(a, blob);
   return cudaGetLastError();
+}
+
+template <typename T, int P, bool W>
+cudaError_t launch_walk(const WalkJob& job, WalkPlan* plan, cudaStream_t stream) {
+  if constexpr (walk_inline_ok<T, P, W>()) {
+    if (job.inline_host) {
+      if (W ? (job.B > 62 || job.wlen > 63) : job.B > P) return cudaErrorInvalidValue;
+      return launch_walk_impl<T, P, W, true>(job, plan, stream);
+    }
+  }
+  if (job.inline_host) return cudaErrorInvalidValue;
+  return launch_walk_impl<T, P, W, false>(job, plan, stream);
 }
 
 // ---- many square Glynn walks in one launch (batches of n = 17..30) -------

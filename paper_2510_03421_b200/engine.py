@@ -20,6 +20,8 @@ ALG_CODE = {"combinatoric": _lib.ALG_COMBINATORIC, "ryser": _lib.ALG_RYSER, "gly
 
 def _stage(a):
     """(pointer, lda, dev_ptr, keepalive, stream) for a 2-D array or tensor."""
+    if isinstance(a, np.ndarray) and a.flags.c_contiguous:  # the common case, no torch lookup
+        return C.c_void_p(a.ctypes.data), a.shape[1], 0, a, None
     try:
         import torch
 
@@ -45,17 +47,24 @@ def _kind(a) -> str:
     return "f" if a.is_floating_point() else "i"
 
 
+_WALK_FN = {}  # (alg, complex) -> bound C entry point
+
+
 def walk(alg: str, a, magsum: bool = False):
     """Glynn / Ryser permanent of a float64 or complex128 m x n (m <= n)
     matrix; returns (value, M) with M the magnitude sum (or None)."""
-    lib = _lib.load()
     cplx = _kind(a) == "c"
     m, n = a.shape
     ptr, lda, dev, keep, stream = _stage(a)
     out = _lib.out_buf(2)
-    mg = C.c_double(0.0)
-    fn = getattr(lib, f"perm_{alg}_{'c128' if cplx else 'f64'}")
-    st = fn(m, n, ptr, lda, dev, out, C.byref(mg) if magsum else None, stream)
+    fn = _WALK_FN.get((alg, cplx))
+    if fn is None:
+        fn = _WALK_FN[(alg, cplx)] = getattr(_lib.load(), f"perm_{alg}_{'c128' if cplx else 'f64'}")
+    if magsum:
+        mg = C.c_double(0.0)
+        st = fn(m, n, ptr, lda, dev, out, C.byref(mg), stream)
+    else:
+        st = fn(m, n, ptr, lda, dev, out, None, stream)
     _lib.check(st, f"{alg} {m}x{n}")
     val = complex(out[0], out[1]) if cplx else float(out[0])
     return val, (mg.value if magsum else None)

@@ -226,12 +226,19 @@ def test_opt_selection_policy(monkeypatch):
         picked.clear()
         D.permanent_opt(np.ones((m, n)))
         assert picked == [D.select_algorithm(m, n, D.b200_params())]
-    for (m, n), want in (((8, 62), D.AlgorithmId.RYSER), ((2, 70), D.AlgorithmId.COMBINATORIC),
-                         ((36, 36), D.AlgorithmId.GLYNN), ((30, 40), D.AlgorithmId.GLYNN)):
+    for (m, n), want in (((8, 62), D.AlgorithmId.RYSER), ((36, 36), D.AlgorithmId.GLYNN),
+                         ((30, 40), D.AlgorithmId.GLYNN)):
         picked.clear()
         D.permanent_opt(np.ones((m, n)))
         assert picked == [want], (m, n)
         assert D.engine_choice(m, n, D.b200_params()) is want
+    # 2 x 70: combinatoric (4830 permutations) or combination-order Ryser
+    # (2485 subsets), never the 2^69-step Glynn walk
+    picked.clear()
+    D.permanent_opt(np.ones((2, 70)))
+    assert picked and picked[0] is not D.AlgorithmId.GLYNN
+    ops = {a: D.walk_ops(a, 2, 70) for a in D.AlgorithmId}
+    assert ops[picked[0]] <= 16 * min(ops.values())
     picked.clear()
     D.permanent_opt(np.ones((8, 62)), params=D.b200_params())  # explicit params: the pure rule
     assert picked == [D.select_algorithm(8, 62, D.b200_params())]

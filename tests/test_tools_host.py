@@ -112,10 +112,14 @@ def test_reference_procedure_on_recorded_b200_timings():
     from paper_2510_03421_b200.dispatch import b200_params, default_params
     from conftest import ROOT
 
-    raw = json.loads((ROOT / "profiles" / "r1_dispatch_timings.json").read_text())
+    raw = json.loads((ROOT / "profiles" / "r2_dispatch_timings.json").read_text())
     t = {tuple(int(x) for x in k.split(",")): v for k, v in raw.items()}
     rep = T.run_tuning(timings=t)
-    assert T._total_slowdown(rep.params, t) <= T._total_slowdown(default_params(), t) * 0.9
+    # beats the reference's CPU table in total and keeps every cell within
+    # the 1.25x acceptance bar (the CPU table's worst cell is 2.5x here)
+    assert T._total_slowdown(rep.params, t) <= T._total_slowdown(default_params(), t) * 0.95
+    worst = max(t[k][select_algorithm(*k, rep.params).value] / min(t[k].values()) for k in t)
+    assert worst <= 1.25
     shipped = b200_params()
     assert shipped.as_list() == rep.params.as_list()
     grid = T.label_grid(t)
