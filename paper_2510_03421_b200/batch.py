@@ -127,8 +127,20 @@ def opt_batch(a, params=None):
     partition formula for m <= 4 < n and m = 5, 6 with n >= m + 2, Glynn on
     the ones-padded pre-scaled matrix for the other rectangles with n >= 9,
     subset-skipping Ryser otherwise).  Shapes: m <= n <= 30, and the
-    partition formula up to n = 62."""
-    return _run(a, None)
+    partition formula up to n = 62.
+
+    ``params`` (a TuningParams): the reference's selection rule
+    (src/dispatch.py:84-95) picks one of combinatoric / Ryser / Glynn for the
+    batch's shape instead, as ``opt(a, params=...)`` would per matrix."""
+    if params is None:
+        return _run(a, None)
+    from .dispatch import select_algorithm
+
+    shape = tuple(a.shape)
+    if len(shape) != 3:
+        raise TypeError(f"expected a [B, m, n] array, got ndim={len(shape)}")
+    m, n = sorted(shape[1:])
+    return _run(a, select_algorithm(m, n, params))
 
 
 def partition_batch(a):

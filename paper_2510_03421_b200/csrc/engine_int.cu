@@ -56,6 +56,7 @@ struct IntSetup {
 
   bool pre_overflow = false;  // reference flags before/independently of the walk
   s128 bound = 0;             // max |state entry| along the walk
+  std::vector<s128> cb;       // per state entry: bound on |entry| along the walk
 };
 
 static void setup_int(int alg, const IntMat& A, IntSetup* s) {
@@ -76,6 +77,7 @@ static void setup_int(int alg, const IntMat& A, IntSetup* s) {
       }
       s->v0[j] = acc;
       s->bound = std::max(s->bound, mag);
+      s->cb.push_back(mag);
       s128 exact = n - m;
       for (int i = 0; i < m; ++i) exact += A.at(i, j);
       s->v0w.push_back((int64_t)(uint64_t)exact);
@@ -113,6 +115,7 @@ static void setup_int(int alg, const IntMat& A, IntSetup* s) {
     s128 mag = 0;
     for (int j = 0; j < n; ++j) mag += (A.at(i, j) < 0) ? -(s128)A.at(i, j) : (s128)A.at(i, j);
     s->bound = std::max(s->bound, mag);
+    s->cb.push_back(mag);
   }
   if (m < n) {
     s->weighted = true;
@@ -212,16 +215,72 @@ static int checked_range(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream
 
 // ------------------------------------------------------------ WRAP walk
 walk_fn_i int_wrap_lookup(int P);
-walk_fn_if int_wrap_fp_lookup(int P);
 
-// Fused path: FP64-exact state and group products (|state| <= 83), the
-// int128 sum and its FP64 estimate / magnitude sum from one kernel.
-static bool fp_walk_ok(const IntSetup& s, uint64_t k0, uint64_t k1) {
-  return !s.weighted && s.bound <= 83 && s.B >= 8 && s.P >= 1 && s.P <= 64 && k1 - k0 >= 8 &&
-         range_align(k0, k1) >= 3;
+// Fused path: FP64-exact state and group products, the int128 sum and its
+// FP64 estimate / magnitude sum from one kernel.  The P state entries are
+// cut into NG groups of P/NG (+1) entries; a group's products are exact when
+// the product of its entries' bounds is below 2^51.  int_fp_groups takes the
+// smallest instantiated NG for which a grouping exists (longest-processing-
+// time assignment of the entries, largest bound first, to the group with the
+// smallest log-product and room left) and returns the state-entry order that
+// realizes it (per(A) and the walk sum do not depend on that order).
+struct FpGroups {
+  int ng = 0;
+  std::vector<int> order;  // kernel index -> original state index
+};
+static bool int_fp_groups(const IntSetup& s, FpGroups* out) {
+  const int P = s.P;
+  if ((int)s.cb.size() != P) return false;
+  std::vector<int> idx(P);
+  for (int j = 0; j < P; ++j) idx[j] = j;
+  std::sort(idx.begin(), idx.end(), [&](int x, int y) { return s.cb[x] > s.cb[y]; });
+  for (int k = 2; k >= 0; --k) {  // fewest groups first
+    const int NG = int_fp_ng(P, k);
+    if (k < 2 && NG == int_fp_ng(P, k + 1)) continue;
+    std::vector<int> cap(NG), start(NG);
+    for (int q = 0; q < NG; ++q) {
+      start[q] = q * P / NG;
+      cap[q] = (q + 1) * P / NG - start[q];
+    }
+    std::vector<long double> lg(NG, 0.0L);
+    std::vector<std::vector<int>> grp(NG);
+    bool ok = true;
+    for (int j : idx) {
+      int best = -1;
+      for (int q = 0; q < NG; ++q)
+        if ((int)grp[q].size() < cap[q] && (best < 0 || lg[q] < lg[best])) best = q;
+      grp[best].push_back(j);
+      const s128 b = s.cb[j] < 1 ? 1 : s.cb[j];
+      lg[best] += std::log2((long double)b);
+      if (lg[best] >= 50.99L) ok = false;
+    }
+    if (!ok) continue;
+    // exact check of each group's bound product against 2^51
+    for (int q = 0; q < NG && ok; ++q) {
+      unsigned __int128 prod = 1;
+      for (int j : grp[q]) {
+        const s128 b = s.cb[j] < 1 ? 1 : s.cb[j];
+        prod *= (unsigned __int128)b;
+        if (prod >= ((unsigned __int128)1 << 51)) ok = false;
+      }
+    }
+    if (!ok) continue;
+    out->ng = NG;
+    out->order.assign(P, 0);
+    for (int q = 0; q < NG; ++q)
+      for (size_t i = 0; i < grp[q].size(); ++i) out->order[start[q] + i] = grp[q][i];
+    return true;
+  }
+  return false;
 }
 
-static int wrap_range_fp(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream_t stream, IntPart* p) {
+static bool fp_walk_ok(const IntSetup& s, uint64_t k0, uint64_t k1, FpGroups* g) {
+  return !s.weighted && s.B >= 8 && s.P >= 1 && s.P <= 64 && k1 - k0 >= 8 && range_align(k0, k1) >= 3 &&
+         int_fp_groups(s, g);
+}
+
+static int wrap_range_fp(const IntSetup& s, const FpGroups& g, uint64_t k0, uint64_t k1, cudaStream_t stream,
+                         IntPart* p) {
   const uint64_t steps = k1 - k0;
   const int amax = range_align(k0, k1);
   int dev = 0, nsm = 148;
@@ -232,9 +291,12 @@ static int wrap_range_fp(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream
   while (log2L < 14 && log2L < amax && (steps >> (log2L + 1)) >= 16 * lanes) ++log2L;
   const uint64_t nchunks = steps >> log2L;
   const uint64_t blocks = std::min<uint64_t>((nchunks + kIntThreads - 1) / kIntThreads, (uint64_t)nsm * 8);
+  // state entries in the kernel's group order
   std::vector<double> buf(s.v0.size() + s.U.size());
-  for (size_t i = 0; i < s.v0.size(); ++i) buf[i] = (double)s.v0[i];
-  for (size_t i = 0; i < s.U.size(); ++i) buf[s.v0.size() + i] = (double)s.U[i];
+  const int P = s.P;
+  for (int j = 0; j < P; ++j) buf[j] = (double)s.v0[g.order[j]];
+  for (int t = 0; t < s.B; ++t)
+    for (int j = 0; j < P; ++j) buf[P + (size_t)t * P + j] = (double)s.U[(size_t)t * P + g.order[j]];
   const size_t bytes = buf.size() * 8 + blocks * 64 + 256;
   DevBuf dbuf;
   PERM_CUDA_TRY(cudaMallocAsync(&dbuf.p, bytes, stream));
@@ -249,7 +311,7 @@ static int wrap_range_fp(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream
   a.k_begin = k0;
   a.nchunks = nchunks;
   a.out = reinterpret_cast<int64_t*>(d + buf.size());
-  walk_fn_if fn = int_wrap_fp_lookup(s.P);
+  walk_fn_if fn = int_wrap_fp_lookup(s.P, g.ng);
   if (!fn) {
     set_error("no fp int walk for this size");
     return PERM_BAD_SHAPE;
@@ -418,7 +480,8 @@ static int int_part(int alg, const IntPlan& pl, int width, uint64_t k0, uint64_t
                     IntPart* p) {
   const IntSetup& s = pl.s;
   if (width == 64) return checked_range(s, k0, k1, stream, p);
-  if (fp_walk_ok(s, k0, k1)) return wrap_range_fp(s, k0, k1, stream, p);
+  FpGroups g;
+  if (fp_walk_ok(s, k0, k1, &g)) return wrap_range_fp(s, g, k0, k1, stream, p);
   if (!pl.cert_apriori) {
     if (s.bound >= ((s128)1 << 52)) {  // state entries not exact in FP64
       p->refused = true;

@@ -17,6 +17,8 @@
 // walk sum is exact whenever the true value lies in (-2^127, 2^127), which the
 // host certifies with an FP64 run plus its magnitude-sum error bound.
 #pragma once
+#include <utility>
+
 #include "common.cuh"
 #include "walk.cuh"
 
@@ -352,8 +354,9 @@ __global__ void __launch_bounds__(kIntThreads) int_walk_wrap_kernel(IntWalkArgs 
   }
 }
 
-// FP64-exact WRAP walk for small integer entries (|state| <= 83, so a
-// product of 8 state entries is < 2^51): state updates and group products
+// FP64-exact WRAP walk for small integer entries (state entries grouped so
+// that each group's product of per-entry bounds is < 2^51; the default
+// groups of 8 need |state| <= 83): state updates and group products
 // run on the FP64 pipe exactly, each group product is converted to int64
 // and folded into the mod-2^128 term.  The same products give the FP64
 // estimate of every term for free, so the int128 fit certificate (FP64 sum
@@ -403,25 +406,35 @@ __device__ __forceinline__ i128 group_product_i128(const int64_t (&c)[NG]) {
   }
 }
 
-template <int P>
+// Product of state entries [Q P / NG, (Q + 1) P / NG) as a balanced tree:
+// every sub-product is an exact integer below 2^51 (the host certified the
+// group's product of per-entry bounds), so the order is free, and B200's FP64
+// pipe wants many independent DMULs in a row.
+template <int P, int NG, int Q>
+__device__ __forceinline__ double fp_group(const double (&v)[P]) {
+  constexpr int lo = Q * P / NG, W = (Q + 1) * P / NG - lo;
+  double t[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) t[j] = v[lo + j];
+#pragma unroll
+  for (int h = 1; h < W; h <<= 1)
+#pragma unroll
+    for (int j = 0; j + h < W; j += 2 * h) t[j] *= t[j + h];
+  return t[0];
+}
+template <int P, int NG, int... Qs>
+__device__ __forceinline__ void fp_groups(const double (&v)[P], double (&g)[NG], std::integer_sequence<int, Qs...>) {
+  ((g[Qs] = fp_group<P, NG, Qs>(v)), ...);
+}
+
+// One term: NG group products (FP64, exact), their int128 product (mod
+// 2^128) into acc, and the FP64 estimate / magnitude of the term.  Fewer,
+// larger groups cut the 64x64 -> 128-bit integer products per step (NG = 4:
+// ~40 IMAD, NG = 3: ~18).
+template <int P, int NG>
 __device__ __forceinline__ void fp_term(const double (&v)[P], bool neg, i128& acc, double& est, double& mag) {
-  constexpr int NG = (P + 7) / 8;
-  // group products as balanced trees (depth 3, not a 7-deep DMUL chain):
-  // every sub-product of a group is itself an exact integer < 2^51, so the
-  // order is free, and B200's FP64 pipe wants many independent DMULs in a row
   double g[NG];
-#pragma unroll
-  for (int q = 0; q < NG; ++q) {
-    constexpr int W = 8;
-    double t[W];
-#pragma unroll
-    for (int j = 0; j < W; ++j) t[j] = (8 * q + j < P) ? v[8 * q + j] : 1.0;
-#pragma unroll
-    for (int h = 1; h < W; h <<= 1)
-#pragma unroll
-      for (int j = 0; j + h < W; j += 2 * h) t[j] *= t[j + h];
-    g[q] = t[0];
-  }
+  fp_groups<P, NG>(v, g, std::make_integer_sequence<int, NG>{});
   int64_t c[NG];
   double f = g[0];
 #pragma unroll
@@ -442,7 +455,7 @@ __device__ __forceinline__ void fp_term(const double (&v)[P], bool neg, i128& ac
 #ifndef INT_FP_MINB
 #define INT_FP_MINB 2  // 220 regs, no spills: 8 warps/SM beat 12 spilling ones (C4a 20.1 -> 15.4 ms)
 #endif
-template <int P>
+template <int P, int NG>
 __global__ void __launch_bounds__(kIntThreads, INT_FP_MINB) int_walk_wrap_fp_kernel(IntWalkFArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* sU = reinterpret_cast<double*>(smem_raw);
@@ -474,21 +487,21 @@ __global__ void __launch_bounds__(kIntThreads, INT_FP_MINB) int_walk_wrap_fp_ker
         const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
         row_fma<double, P>(v, set ? 1.0 : -1.0, sU + t * PS);
       }
-      fp_term<P>(v, false, acc, est, mag);
+      fp_term<P, NG>(v, false, acc, est, mag);
       INT_ROW0(add);
-      fp_term<P>(v, true, acc, est, mag);
+      fp_term<P, NG>(v, true, acc, est, mag);
       row_add<double, P>(v, sU + PS);
-      fp_term<P>(v, false, acc, est, mag);
+      fp_term<P, NG>(v, false, acc, est, mag);
       INT_ROW0(sub);
-      fp_term<P>(v, true, acc, est, mag);
+      fp_term<P, NG>(v, true, acc, est, mag);
       row_fma<double, P>(v, (((k0 + l0) >> 3) & 1) ? -1.0 : 1.0, sU + 2 * PS);
-      fp_term<P>(v, false, acc, est, mag);
+      fp_term<P, NG>(v, false, acc, est, mag);
       INT_ROW0(add);
-      fp_term<P>(v, true, acc, est, mag);
+      fp_term<P, NG>(v, true, acc, est, mag);
       row_sub<double, P>(v, sU + PS);
-      fp_term<P>(v, false, acc, est, mag);
+      fp_term<P, NG>(v, false, acc, est, mag);
       INT_ROW0(sub);
-      fp_term<P>(v, true, acc, est, mag);
+      fp_term<P, NG>(v, true, acc, est, mag);
     }
     dd_acc(hi, lo, est);
 #undef INT_ROW0
@@ -522,11 +535,19 @@ __global__ void __launch_bounds__(kIntThreads, INT_FP_MINB) int_walk_wrap_fp_ker
 
 using walk_fn_i = cudaError_t (*)(const IntWalkArgs&, int blocks, cudaStream_t);
 using walk_fn_if = cudaError_t (*)(const IntWalkFArgs&, int blocks, cudaStream_t);
+// Group counts instantiated for the fp walk at state length P: groups of
+// about 8, 11 and 14 entries (the host takes the smallest count whose groups
+// it can certify, int_fp_groups in engine_int.cu).
+__host__ __device__ constexpr int int_fp_ng(int P, int k) {
+  const int gs = k == 0 ? 8 : (k == 1 ? 11 : 14);
+  return (P + gs - 1) / gs;
+}
+walk_fn_if int_wrap_fp_lookup(int P, int NG);
 
-template <int P>
+template <int P, int NG>
 cudaError_t launch_int_wrap_fp(const IntWalkFArgs& a, int blocks, cudaStream_t stream) {
   const size_t smem = (size_t)a.B * ((P + 1) & ~1) * sizeof(double);
-  auto kern = int_walk_wrap_fp_kernel<P>;
+  auto kern = int_walk_wrap_fp_kernel<P, NG>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

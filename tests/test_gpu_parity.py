@@ -362,6 +362,23 @@ def test_batch_complex_and_device(rng):
     assert P.opt_batch(np.zeros((0, 4, 4))).shape == (0,)
 
 
+def test_opt_batch_params_follow_the_selection_rule(rng):
+    """opt_batch(params=...) runs the algorithm the reference's rule picks
+    for the shape (ADVICE/VERDICT r1 W10: params used to be ignored)."""
+    from paper_2510_03421_b200.dispatch import default_params, select_algorithm
+
+    d = default_params()
+    for (m, n) in ((4, 4), (3, 9), (10, 10)):
+        A = rng.uniform(-1, 1, (40, m, n))
+        out = P.opt_batch(A, params=d)
+        alg = select_algorithm(m, n, d)
+        ref = {"combinatoric": P.combinatoric_batch, "ryser": P.ryser_batch, "glynn": P.glynn_batch}[alg.value](A)
+        assert np.array_equal(out, ref), (m, n, alg)
+        for i in (0, 17, 39):
+            r = O.permanent(alg.value, A[i])[0]
+            assert scaled_err(out[i], r, magsum(A[i])) <= TOL
+
+
 def test_c1_batch_warp_per_matrix():
     """64 x 12x12 (C1) through the batch API: small batches of n >= 9 run one
     warp per matrix; results must match the reference like the per-matrix
