@@ -70,6 +70,14 @@ int perm_fp64_peak_probe(double seconds, double* dfma_per_s);
  * instruction mix -- on B200 it reaches the nominal 64 op/clk/SM while DFMA
  * tops out ~8% lower, so the walk's FP64-pipe roofline is op 1's figure. */
 int perm_fp64_pipe_probe(int op, double seconds, double* ops_per_s);
+/* Measurement: device time of the float Gray walk of one host matrix
+ * (alg GLYNN / RYSER, cplx 0/1), launched `reps` times back to back on a
+ * private stream after one warm-up -- the setup is built once, so the
+ * figure is the kernel's per-permanent device time including the
+ * launch-to-launch gap, without the per-call host work.  *ms_per_launch
+ * receives the CUDA-event time divided by reps. */
+int perm_walk_repeat_ms(int alg, int cplx, int m, int n, const double* a, int64_t lda, int reps,
+                        double* ms_per_launch);
 
 /* ---- single permanents, float64 / complex128 --------------------------
  * Replace glynn_sq/glynn_rect + permanent_glynn_{square,rectangular}

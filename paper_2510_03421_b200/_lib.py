@@ -36,6 +36,7 @@ SIGNATURES = {
     "perm_last_kernel_plan": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "perm_fp64_peak_probe": (C.c_int, [C.c_double, _dp]),
     "perm_fp64_pipe_probe": (C.c_int, [C.c_int, C.c_double, _dp]),
+    "perm_walk_repeat_ms": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp]),
     "perm_glynn_f64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _dp, _vp]),
     "perm_glynn_c128": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _dp, _vp]),
     "perm_ryser_f64": (C.c_int, [C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _dp, _dp, _vp]),

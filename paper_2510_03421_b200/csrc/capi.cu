@@ -499,6 +499,51 @@ int perm_fp64_pipe_probe(int op, double seconds, double* ops_per_s) {
   return fp64_peak_probe(seconds, op, ops_per_s);
 }
 
+int perm_walk_repeat_ms(int alg, int cplx, int m, int n, const double* a, int64_t lda, int reps,
+                        double* ms_per_launch) {
+  clear_error();
+  if ((alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER) || reps < 1 || !ms_per_launch) {
+    set_error("alg must be GLYNN or RYSER, reps >= 1");
+    return PERM_BAD_ARG;
+  }
+  int st = check_shape(alg, m, n);
+  if (st) return st;
+  HostMat A;
+  st = load_matrix(m, n, a, lda, 0, cplx != 0, &A, nullptr);
+  if (st) return st;
+  WalkSetup ws;
+  st = build_walk(alg, A, &ws, /*exact_state=*/true);
+  if (st) return st;
+  Scratch* s = scratch();
+  if (!s) return cuda_fail(cudaErrorNoDevice, "scratch");
+  cudaStream_t stream;
+  PERM_CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  const size_t part_bytes = (size_t)kMaxPartials * kPartialStride * sizeof(double);
+  st = ensure_dev(s, part_bytes + ws.buf.size() * sizeof(double) + 64 * sizeof(double) + 256);
+  if (st) return st;
+  double* dst = reinterpret_cast<double*>(static_cast<char*>(s->dev) + s->dev_cap) - 8;
+  const uint64_t steps = walk_steps(alg, m, n);
+  st = run_walk(ws, 0, steps, 0, dst, stream);  // warm-up (and the setup's first upload)
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (!st) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, stream);
+    for (int r = 0; r < reps && !st; ++r) st = run_walk_resident(ws, 0, steps, 0, dst, stream);
+    cudaEventRecord(e1, stream);
+  }
+  const cudaError_t se = cudaStreamSynchronize(stream);
+  float ms = 0.0f;
+  if (!st && se == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  cudaStreamDestroy(stream);
+  if (st) return st;
+  if (se != cudaSuccess) return cuda_fail(se, "walk repeat");
+  *ms_per_launch = (double)ms / reps;
+  return PERM_OK;
+}
+
 int perm_device_sm_count(void) {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;

@@ -390,7 +390,8 @@ static bool walk_inline_fits(const WalkSetup& ws) {
 }
 
 static int launch_setup(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst,
-                        unsigned int* flag, unsigned int seq, bool allow_inline, cudaStream_t stream) {
+                        unsigned int* flag, unsigned int seq, bool allow_inline, cudaStream_t stream,
+                        bool upload = true) {
   if (ws.P < 1 || ws.P > 64) {
     set_error("state length out of range (1..64)");
     return PERM_BAD_SHAPE;
@@ -408,7 +409,7 @@ static int launch_setup(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, i
   double* data = partials + (size_t)kMaxPartials * kPartialStride;
   const uint64_t steps = k_end - k_begin;
   const bool inl = allow_inline && (walk_tiled(k_begin, steps) || (steps > 0 && steps < 256)) && walk_inline_fits(ws);
-  if (!inl) {
+  if (!inl && upload) {
     st = stage_h2d(s, data, ws.buf.data(), data_bytes, stream);
     if (st) return st;
   }
@@ -449,6 +450,11 @@ static int launch_setup(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, i
 
 int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst, cudaStream_t stream) {
   return launch_setup(ws, k_begin, k_end, mag, dst, nullptr, 0, true, stream);
+}
+
+int run_walk_resident(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst,
+                      cudaStream_t stream) {
+  return launch_setup(ws, k_begin, k_end, mag, dst, nullptr, 0, true, stream, /*upload=*/false);
 }
 
 static int mapped_slot(Scratch* s) {

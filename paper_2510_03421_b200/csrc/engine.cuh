@@ -84,6 +84,10 @@ int prescale_log2(const HostMat& A);
 void normalize(int alg, int m, int n, int scale_log2, double* re, double* im, double* mag);
 // Run the walk over [k_begin, k_end) -> 8 raw doubles at `dst` (device).
 int run_walk(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst, cudaStream_t stream);
+// The same launch with the setup already resident in the device scratch
+// (an earlier run_walk of this WalkSetup on this thread): no staging copy.
+int run_walk_resident(const WalkSetup& ws, uint64_t k_begin, uint64_t k_end, int mag, double* dst,
+                      cudaStream_t stream);
 // Whole walk with the 8 raw result doubles returned in host memory: the
 // zero-copy path (setup as kernel parameters, result + flag in mapped pinned
 // memory, spin on the flag) where it applies, else run_walk + copy + sync.
