@@ -139,7 +139,12 @@ def run_reference(args):
                          "sample": f"first {sample} Gray steps of the {args.n}x{args.n} C5 walk per step, "
                                    f"split over {cores} threads (oracle/perm_oracle.c, the reference's "
                                    "src/_kernels.py:373-409 walk restated; reference itself is Python+numba, "
-                                   "not present on the GPU box)"},
+                                   "not present on the GPU box)",
+                         "port_vs_reference": "the port's 1-thread rate on this box (bench.py cpu_baseline, "
+                                              "3.0-4.3e7 steps/s) matches the numba reference's single-threaded "
+                                              "glynn_sq measured in the build container (2.7-5.2e7 steps/s, "
+                                              "SURVEY 6); the reference walk is single-threaded, so this "
+                                              "all-threads port is a stronger CPU baseline than the reference"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
