@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(TPB, MINB) batch_bulk_kernel(const T* __restri
         }
       }
     };
+    PERM_CHECK(cnt >= 1 && cnt <= MATS && first + cnt <= nb);
     Op::run(reinterpret_cast<const T*>(bb_smem_raw + (size_t)slot * TILE_BYTES), first, cnt, out, threadIdx.x,
             release);
     if (++slot == STAGES) {
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) batch_bulk_warp_kernel(const
         }
       }
     };
+    PERM_CHECK(cnt >= 1 && cnt <= MATS && first + cnt <= nb);
     Op::run(reinterpret_cast<const T*>(ring + (size_t)slot * TILE_BYTES), first, cnt, out, lane, release);
     if (++slot == STAGES) {
       slot = 0;

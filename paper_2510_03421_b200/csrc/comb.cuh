@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kCombThreads) ryser_comb_kernel(CombArgs A) {
         if (r < cnt) { comb[q] = x++; break; }
         r -= cnt;
         ++x;
+        PERM_CHECK(x < n);  // the rank lies inside C(n, s)
       }
     }
     if constexpr (MODE == kCombI64) {
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
   const uint64_t p0 = gtid * A.per_thread;
   uint64_t p1 = p0 + A.per_thread;
   if (p1 > A.total) p1 = A.total;
+  PERM_CHECK(D >= 1 && D <= m && m <= 64 && n <= kCombMaxN);
   for (uint64_t pidx = p0; pidx < p1 && !sm.flag; ++pidx) {
     // decode prefix: mixed radix (n, n-1, ..., n-D+1), most significant first
     int choice[64];

@@ -7,7 +7,28 @@
 // * 128-bit two's-complement helpers for the exact integer path.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Bounds-assert build mode (`make debug` -> libpermanent_b200_debug.so,
+// -DPERM_DEBUG_BOUNDS): PERM_CHECK traps with the failing condition and its
+// source line; compute-sanitizer is closed on this GPU pool, so the debug
+// library runs the GPU parity tests instead (tools/debug_bounds_check.sh).
+// Compiled out otherwise.
+#ifdef PERM_DEBUG_BOUNDS
+#define PERM_CHECK(cond)                                                                      \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("PERM_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                              \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define PERM_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 namespace permb200 {
 

@@ -474,6 +474,7 @@ __global__ void __launch_bounds__(kIntThreads, INT_FP_MINB) int_walk_wrap_fp_ker
     const uint64_t k0 = a.k_begin + (c << a.log2L);
     double v[P];
     const uint64_t g0 = k0 ^ (k0 >> 1);
+    PERM_CHECK(a.log2L >= 3 && a.log2L <= B && (B >= 63 || (k0 >> B) == 0));
 #pragma unroll
     for (int j = 0; j < P; ++j) v[j] = a.v0[j];
     for (int t = 0; t < B; ++t)

@@ -68,6 +68,7 @@ __device__ __forceinline__ void walk_last_block_combine(const double* partials, 
                                                         unsigned int* done, unsigned int* flag = nullptr,
                                                         unsigned int seq = 0) {
   __shared__ bool last;
+  PERM_CHECK(gridDim.x <= (unsigned)(148 * 16));  // kMaxPartials partial slots
   if (threadIdx.x == 0) {
     __threadfence();
     last = (atomicAdd(done, 1u) == gridDim.x - 1);
@@ -530,6 +531,7 @@ __device__ __forceinline__ void walk_group_range(const T* sU, const T* sV0, T* m
   const uint64_t nq = L >> 3;
   const uint64_t bmask = (B >= 64) ? ~0ull : ((1ull << B) - 1);
   const uint64_t hmask = (~0ull << (log2L + 5)) & bmask;  // warp-uniform Gray bits
+  PERM_CHECK(log2L >= 3 && log2L <= B);  // in-chunk flip rows ctz(l) < log2L must be rows of U
   for (uint64_t g = g_first; g < g_end; g += g_stride) {
     const uint64_t kb = k_begin + ((g * 32) << log2L);
     const uint64_t k0 = kb + ((uint64_t)lane << log2L);
@@ -542,6 +544,7 @@ __device__ __forceinline__ void walk_group_range(const T* sU, const T* sV0, T* m
         while (bits) {
           int t = __ffsll((long long)bits) - 1;
           bits &= bits - 1;
+          PERM_CHECK(t < B);
           acc = Num<T>::add(acc, sU[t * PS + j]);
         }
         myWarp[j] = acc;
@@ -678,7 +681,10 @@ __device__ __forceinline__ void walk_stage(const T* __restrict__ src, int B, T* 
     for (int k = 0; k < 4; ++k) {
       const int e = base + k * kWalkThreads + (int)threadIdx.x;
       if (e < P) sV0[e] = r[k];
-      else if (e < total) sU[(e / P - 1) * PS + (e % P)] = r[k];
+      else if (e < total) {
+        PERM_CHECK(e / P - 1 < B);
+        sU[(e / P - 1) * PS + (e % P)] = r[k];
+      }
     }
   }
 }
@@ -755,6 +761,7 @@ __global__ void __launch_bounds__(kWalkThreads, walk_min_blocks<T, P>()) walk_mu
   for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
     const int64_t mat = w / args.segs;
     const int seg = (int)(w - mat * args.segs);
+    PERM_CHECK(mat < args.nmats && seg < args.segs);
     const int m = args.m;
     const T* A = static_cast<const T*>(args.a) + mat * m * P;
     __syncthreads();  // previous item's shared memory is free
@@ -860,6 +867,7 @@ __global__ void __launch_bounds__(32) walk_tiny_kernel(WalkArgs args, const __gr
   const uint64_t g0 = k0 ^ (k0 >> 1);
 #pragma unroll
   for (int j = 0; j < P; ++j) v[j] = v0[j];
+  PERM_CHECK(args.B <= 62 && (args.B == 0 || k_end <= (1ull << args.B)));
   for (int t = 0; t < args.B; ++t)
     if ((g0 >> t) & 1) {
 #pragma unroll
@@ -872,6 +880,7 @@ __global__ void __launch_bounds__(32) walk_tiny_kernel(WalkArgs args, const __gr
     if (k != k0) {
       const int t = __ffsll((long long)k) - 1;
       const int set = (int)(((k ^ (k >> 1)) >> t) & 1);
+      PERM_CHECK(t < args.B);
 #pragma unroll
       for (int j = 0; j < P; ++j) v[j] = set ? Num<T>::add(v[j], U[t * P + j]) : Num<T>::sub(v[j], U[t * P + j]);
       pc += set ? 1 : -1;
