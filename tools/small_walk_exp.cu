@@ -222,7 +222,64 @@ void walk_exp(double* d_part, double* d_final, unsigned* d_done, double* d_data)
   cudaStreamDestroy(s);
 }
 
+// N24=1: the n = 24 walk over forced chunk lengths (and whatever WALK_*
+// macros this binary was built with)
+template <int P>
+void chunk_sweep(double* d_part, double* d_final, unsigned* d_done, double* d_data) {
+  const int B = P - 1;
+  std::vector<double> a((size_t)P * P), buf((size_t)P + (size_t)B * P);
+  unsigned long long x = 88172645463325252ull + P;
+  for (auto& v : a) {
+    x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+    v = (double)(x >> 11) * 0x1.0p-53 / P;
+  }
+  for (int j = 0; j < P; ++j) {
+    double c = 0;
+    for (int i = 0; i < P; ++i) c += a[(size_t)i * P + j];
+    buf[j] = c;
+  }
+  for (int t = 0; t < B; ++t)
+    for (int j = 0; j < P; ++j) buf[P + (size_t)t * P + j] = -2.0 * a[(size_t)(P - 1 - t) * P + j];
+  cudaMemcpy(d_data, buf.data(), buf.size() * 8, cudaMemcpyHostToDevice);
+  cudaStream_t s;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  WalkJob job{};
+  job.P = P; job.B = B; job.v0 = d_data; job.U = d_data + P; job.k_begin = 0; job.k_end = 1ull << B;
+  job.partials = d_part; job.final_out = d_final; job.done = d_done;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int r : {0, 4, 5, 6, 7, 8}) {
+    job.force_log2L = r;
+    WalkPlan plan;
+    for (int i = 0; i < 20; ++i) launch_walk<double, P, false>(job, &plan, s);
+    cudaEventRecord(e0, s);
+    for (int i = 0; i < 200; ++i) launch_walk<double, P, false>(job, &plan, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double us = 1e3 * ms / 200;
+    printf("P=%d r0=%d log2L %d%s grid %d: %.2f us (pipe %.1f%%)\n", P, (int)walk_r0<double, P>(), plan.log2L,
+           r ? "" : " (model)", plan.grid, us, 100.0 * (double)(1ull << B) * 2 * P / (us * 1e-6) / (148 * 64 * 1.965e9));
+  }
+}
+
 int main() {
+  if (getenv("N24")) {
+    double *d_part, *d_final, *d_data;
+    unsigned* d_done;
+    cudaMalloc(&d_part, (size_t)kMaxPartials * kPartialStride * 8);
+    cudaMalloc(&d_final, 64);
+    cudaMalloc(&d_data, 1 << 20);
+    cudaMalloc(&d_done, 4);
+    cudaMemset(d_done, 0, 4);
+    chunk_sweep<22>(d_part, d_final, d_done, d_data);
+    chunk_sweep<23>(d_part, d_final, d_done, d_data);
+    chunk_sweep<24>(d_part, d_final, d_done, d_data);
+    chunk_sweep<25>(d_part, d_final, d_done, d_data);
+    return 0;
+  }
   if (getenv("BIG")) {
     double *d_part, *d_final, *d_data;
     unsigned* d_done;
