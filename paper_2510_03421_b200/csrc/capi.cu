@@ -90,9 +90,39 @@ bool ryser_rect_use_comb(int m, int n) {
   return comb_us < walk_us;
 }
 
+// Every float kernel of the reference starts its sum at zero = a[0,0] -
+// a[0,0] (src/_kernels.py:30, 117, 228, 375, 533), so a non-finite a[0,0]
+// turns the real (imaginary) part of the result into NaN even where the
+// algebra would give +-inf (e.g. combinatoric of [[inf, 1], [1, 1]]).
+// Applied to every float single-permanent result; finite a[0,0] changes
+// nothing (not even the sign of a zero).
+int ref_zero_quirk(bool cplx, const double* a, int dev_ptr, void* stream_, double* out) {
+  double a00[2] = {0.0, 0.0};
+  if (dev_ptr) {
+    cudaStream_t stream = pick_stream(stream_);
+    PERM_CUDA_TRY(cudaMemcpyAsync(a00, a, (cplx ? 2 : 1) * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+  } else {
+    a00[0] = a[0];
+    if (cplx) a00[1] = a[1];
+  }
+  if (!std::isfinite(a00[0])) out[0] += a00[0] - a00[0];
+  if (cplx && !std::isfinite(a00[1])) out[1] += a00[1] - a00[1];
+  return PERM_OK;
+}
+
+int walk_single_impl(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out,
+                     double* magsum, void* stream_);
+
 // Single permanent through the walk engine; returns normalized value.
 int walk_single(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out,
                 double* magsum, void* stream_) {
+  const int st = walk_single_impl(alg, cplx, m, n, a, lda, dev_ptr, out, magsum, stream_);
+  return st ? st : ref_zero_quirk(cplx, a, dev_ptr, stream_, out);
+}
+
+int walk_single_impl(int alg, bool cplx, int m, int n, const double* a, int64_t lda, int dev_ptr, double* out,
+                     double* magsum, void* stream_) {
   clear_error();
   // very rectangular Ryser (and any width past the walks' 62 columns, where
   // the reference's ryser_rect has no cap): the reference's combination order
@@ -196,7 +226,7 @@ int walk_finish(int alg, bool cplx, int m, int n, const double* a, int64_t lda, 
   out[0] = re;
   if (cplx) out[1] = im;
   if (magsum) *magsum = mg;
-  return PERM_OK;
+  return ref_zero_quirk(cplx, a, 0, nullptr, out);
 }
 
 // ---- single-process multi-device driver (perm_sharded_*) ------------------
@@ -595,10 +625,12 @@ int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int
 // ryser_rectangular(square) is the reference's (the square Gray walk checks
 // other intermediates).
 int perm_ryser_rect_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, void* stream) {
-  return comb_permanent(true, 0, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream);
+  const int st = comb_permanent(true, 0, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream);
+  return st ? st : ref_zero_quirk(false, a, dev_ptr, stream, out);
 }
 int perm_ryser_rect_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, void* stream) {
-  return comb_permanent(true, 1, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream);
+  const int st = comb_permanent(true, 1, m, n, a, lda, dev_ptr, UINT64_MAX, out, nullptr, stream);
+  return st ? st : ref_zero_quirk(true, a, dev_ptr, stream, out);
 }
 int perm_ryser_rect_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int64_t* out, void* stream) {
   int64_t v = 0;
@@ -611,11 +643,13 @@ int perm_ryser_rect_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr
 
 int perm_comb_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t step_budget, double* out,
                   void* stream) {
-  return comb_permanent(false, 0, m, n, a, lda, dev_ptr, step_budget, out, nullptr, stream);
+  const int st = comb_permanent(false, 0, m, n, a, lda, dev_ptr, step_budget, out, nullptr, stream);
+  return st ? st : ref_zero_quirk(false, a, dev_ptr, stream, out);
 }
 int perm_comb_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, uint64_t step_budget, double* out,
                    void* stream) {
-  return comb_permanent(false, 1, m, n, a, lda, dev_ptr, step_budget, out, nullptr, stream);
+  const int st = comb_permanent(false, 1, m, n, a, lda, dev_ptr, step_budget, out, nullptr, stream);
+  return st ? st : ref_zero_quirk(true, a, dev_ptr, stream, out);
 }
 int perm_comb_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, uint64_t step_budget,
                   int64_t* out, int* fits_int64, void* stream) {

@@ -132,3 +132,39 @@ def test_repeat_ms_entry_point(rng):
     _lib.check(lib.perm_walk_repeat_ms(_lib.ALG_GLYNN, 0, 20, 20, C.c_void_p(a.ctypes.data), 20, 20, ms), "repeat")
     assert 0.0 < ms[0] < 5.0
     assert lib.perm_walk_repeat_ms(_lib.ALG_COMBINATORIC, 0, 20, 20, C.c_void_p(a.ctypes.data), 20, 20, ms) != 0
+
+
+def _same_special(x, ref):
+    """NaN where the reference has NaN, the same infinities, the same signed
+    zeros, finite values within 1e-12 relative."""
+    import math
+
+    if math.isnan(ref):
+        return math.isnan(x)
+    if math.isinf(ref) or ref == 0.0:
+        return x == ref and math.copysign(1.0, x) == math.copysign(1.0, ref)
+    return abs(x - ref) <= 1e-12 * abs(ref)
+
+
+def test_special_values_match_the_reference():
+    """Non-finite and extreme inputs (tests/golden/special_values.json, made
+    by running the reference: oracle/gen_special.py): the reference starts
+    every float sum at a[0,0] - a[0,0], so a non-finite a[0,0] gives NaN
+    where the algebra gives +-inf; overflow, underflow and Ryser's signed
+    zero follow the same arithmetic."""
+    import json
+
+    from conftest import GOLDEN
+
+    cases = json.loads((GOLDEN / "special_values.json").read_text())
+    for name, c in cases.items():
+        vals = [[complex(x) for x in r] for r in c["matrix"]]  # repr() strings: '-inf', '(inf+1j)', ...
+        a = np.array(vals) if c["complex"] else np.array([[z.real for z in r] for r in vals])
+        for alg in ("combinatoric", "ryser", "glynn"):
+            v = getattr(P, alg)(a)
+            ref = complex(c[alg])
+            if c["complex"]:
+                ok = _same_special(v.real, ref.real) and _same_special(v.imag, ref.imag)
+            else:
+                ok = _same_special(float(v), ref.real)
+            assert ok, (name, alg, v, c[alg])
