@@ -1,14 +1,18 @@
 // Small single walks (n = 14..26): where the time goes.
 //
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo \
-//        -I paper_2510_03421_b200/csrc tools/small_walk_exp.cu -o tools/small_walk_exp_bin
-//   tools/small_walk_exp_bin
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -ffp-contract=off \
+//        -I paper_2510_03421_b200/csrc tools/small_walk_exp.cu -o tools/swx_small      (add -DWALK_TIMELINE
+//        for the per-phase %globaltimer stamps of the walk kernel)
+//   tools/swx_small                    launch floors, then P = 16..36: setup in device memory + D2H copy
+//                                      vs setup as kernel parameters + mapped result flag
+//   SKIP_FLOOR=1 tools/swx_small       the walks only;  BIG=1: P = 30..34;  N24=1: chunk-length sweep
 //
-// Prints (1) launch floors: an empty kernel back to back (device time per
-// launch) and launch -> host-visible round trips (stream sync vs a flag in
-// mapped host memory), with 0 / 4 / 8 / 16 KB of kernel parameters;
-// (2) walk_kernel<double, P> for P = 16..26: device time per launch back to
-// back for every chunk length the plan allows, and the single-call round trip.
+// Launch floors: an empty kernel back to back (device time per launch) and
+// launch -> host-visible round trips (stream sync vs a flag in mapped host
+// memory), with 0 / 4 / 8 / 16 / 30 KB of kernel parameters.  Results:
+// DESIGN 2.3b, profiles/r2_small_walk_probe.txt.  (Variants measured and
+// dropped there: an all-lanes-contiguous work split, per-block partials
+// published straight to host memory.)
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -19,8 +23,7 @@
 using namespace permb200;
 using clk = std::chrono::steady_clock;
 static unsigned *g_hflag, *g_dflag;
-static double *g_hres, *g_dres, *g_hpart, *g_dpart;
-static unsigned *g_hflags, *g_dflags;
+static double *g_hres, *g_dres;
 
 template <int BYTES>
 struct Blob {
@@ -311,11 +314,6 @@ int main() {
   cudaHostGetDevicePointer(&g_dflag, g_hflag, 0);
   cudaHostAlloc(&g_hres, 64, cudaHostAllocMapped);
   cudaHostGetDevicePointer(&g_dres, g_hres, 0);
-  cudaHostAlloc(&g_hpart, kMaxPartials * 64, cudaHostAllocMapped);
-  cudaHostGetDevicePointer(&g_dpart, g_hpart, 0);
-  cudaHostAlloc(&g_hflags, kMaxPartials * 4, cudaHostAllocMapped);
-  memset(g_hflags, 0, kMaxPartials * 4);
-  cudaHostGetDevicePointer(&g_dflags, g_hflags, 0);
   for (int g : {148}) {
     if (getenv("SKIP_FLOOR")) break;
     launch_floor<0>(d_out, hflag, dflag, g);
