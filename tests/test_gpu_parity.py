@@ -710,6 +710,27 @@ def test_randomized_shapes_all_paths():
                     assert scaled_err(out[i], r, magsum2(A[i])) <= TOL, (case, bfn.__name__, m, n, i)
 
 
+def test_randomized_medium_shapes():
+    """The same fuzz for 15 <= n <= 24 single permanents (the zero-copy walk
+    with the setup as kernel parameters, the staged walk past its size
+    limit, the weighted rectangular Ryser and the combination order),
+    against the C double-double oracle; PERM_FUZZ_MEDIUM cases (default 24)."""
+    rng = np.random.default_rng(20261021)
+    laws = [lambda s: rng.uniform(-1, 1, s), lambda s: rng.standard_normal(s), lambda s: rng.uniform(0, 1, s),
+            lambda s: (rng.random(s) < 0.3) * rng.standard_normal(s)]
+    for case in range(int(os.environ.get("PERM_FUZZ_MEDIUM", "24"))):
+        n = int(rng.integers(15, 25))
+        m = int(rng.integers(1, n + 1))
+        law = laws[case % len(laws)]
+        a = law((m, n)) / np.sqrt(n)
+        if case % 3 == 2:
+            a = a + 1j * law((m, n)) / np.sqrt(n)
+        ref = O.dd_permanent("ryser" if m < n else "glynn", a, nthreads=16)
+        for fn in (P.opt, P.glynn, P.ryser):
+            got = fn(a)
+            assert scaled_err(got, ref, magsum2(a)) <= TOL, (case, fn.__name__, m, n, got, ref)
+
+
 def test_integer_batches_exact():
     """Integer batches: certified matrices run on the float batch kernels
     (exact there), the rest per matrix; every value equals the oracle's exact
