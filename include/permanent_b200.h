@@ -85,7 +85,12 @@ int perm_walk_repeat_ms(int alg, int cplx, int m, int n, const double* a, int64_
  * `out` receives the *normalized* permanent (1 double, or re/im for c128).
  * Rectangular Glynn pre-scales the real rows by a power of two
  * (SURVEY 7.4.2), which is exact algebra.  `magsum` (optional, may be NULL)
- * receives M = the normalized sum of |terms|. */
+ * receives M = the normalized sum of |terms|.
+ * stream NULL with a host matrix: the zero-copy route (the walk setup passed
+ * as kernel parameters up to 5.5 KB, the result through mapped pinned memory
+ * and a release-store flag); a caller's stream keeps stream-ordered staged
+ * copies.  Like the reference's kernels, whose sums start at
+ * a[0,0] - a[0,0], a non-finite a[0,0] gives NaN (real / imaginary part). */
 int perm_glynn_f64(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
                    void* stream);
 int perm_glynn_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, double* out, double* magsum,
