@@ -15,9 +15,29 @@ from conftest import ROOT
 
 pytestmark = pytest.mark.gpu
 LIB = ROOT / "paper_2510_03421_b200" / "libpermanent_b200_debug.so"
+STAMP = LIB.with_suffix(".stamp")
 
 
-@pytest.mark.skipif(not LIB.exists(), reason="debug library not built (make -C paper_2510_03421_b200/csrc debug)")
+def _sources_hash() -> str:
+    """sha256 of the engine sources in the order the Makefile's debug target
+    hashes them (csrc/*.cu, *.cuh and the header, sorted by path)."""
+    import hashlib
+
+    csrc = ROOT / "paper_2510_03421_b200" / "csrc"
+    files = sorted([f"{p.name}" for p in csrc.glob("*.cu")] + [f"{p.name}" for p in csrc.glob("*.cuh")] +
+                   ["../../include/permanent_b200.h"])
+    h = hashlib.sha256()
+    for f in files:
+        h.update((csrc / f).read_bytes())
+    return h.hexdigest()
+
+
+def _debug_lib_current() -> bool:
+    return LIB.exists() and STAMP.exists() and STAMP.read_text().strip() == _sources_hash()
+
+
+@pytest.mark.skipif(not _debug_lib_current(),
+                    reason="debug library absent or stale (make -C paper_2510_03421_b200/csrc debug)")
 def test_bounds_checked_library_runs_clean():
     env = dict(os.environ, PERMANENT_B200_LIB=str(LIB))
     code = ("import __graft_entry__ as g; g.smoke(); "
