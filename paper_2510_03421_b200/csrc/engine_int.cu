@@ -128,12 +128,35 @@ static void setup_int(int alg, const IntMat& A, IntSetup* s) {
   }
 }
 
-struct DevBuf {
-  void* p = nullptr;
-  ~DevBuf() {
-    if (p) cudaFree(p);
+
+// One range's inputs go to the thread's device scratch in one pinned-staged
+// copy, and its block outputs come back through the pinned result buffer:
+// per-call cudaMallocAsync / pageable copies cost ~10-15 us of a 40 us
+// small-matrix call (round 2).  Sequential within a call (each range
+// synchronizes before the next uses the scratch).
+static int int_stage(const void* host, size_t in_bytes, size_t out_bytes, cudaStream_t stream, char** d,
+                     size_t* out_off) {
+  Scratch* sc = scratch();
+  if (!sc) return cuda_fail(cudaErrorNoDevice, "scratch");
+  *out_off = (in_bytes + 255) & ~(size_t)255;
+  int st = ensure_dev(sc, *out_off + out_bytes + 256);
+  if (st) return st;
+  *d = static_cast<char*>(sc->dev);
+  return in_bytes ? stage_h2d(sc, *d, host, in_bytes, stream) : PERM_OK;
+}
+static int int_fetch(const void* dout, size_t bytes, cudaStream_t stream, void* host) {
+  Scratch* sc = scratch();
+  if (!sc) return cuda_fail(cudaErrorNoDevice, "scratch");
+  if (bytes <= kHostResultDoubles * sizeof(double)) {
+    PERM_CUDA_TRY(cudaMemcpyAsync(sc->host, dout, bytes, cudaMemcpyDeviceToHost, stream));
+    PERM_CUDA_TRY(cudaStreamSynchronize(stream));
+    std::memcpy(host, sc->host, bytes);
+  } else {
+    PERM_CUDA_TRY(cudaMemcpyAsync(host, dout, bytes, cudaMemcpyDeviceToHost, stream));
+    PERM_CUDA_TRY(cudaStreamSynchronize(stream));
   }
-};
+  return PERM_OK;
+}
 
 // ------------------------------------------------------------ Gray ranges
 // Every integer walk below runs over one Gray range [k0, k1) (the whole walk
@@ -172,12 +195,13 @@ static int checked_range(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream
   const uint64_t nchunks = steps >> log2L;
   const uint64_t blocks = (nchunks + kIntThreads - 1) / kIntThreads;
   const size_t nv0 = s.v0.size(), nU = s.U.size();
-  const size_t bytes = (nv0 + nU) * 8 + blocks * 64;
-  DevBuf buf;
-  PERM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, stream));
-  int64_t* d = static_cast<int64_t*>(buf.p);
-  PERM_CUDA_TRY(cudaMemcpyAsync(d, s.v0.data(), nv0 * 8, cudaMemcpyHostToDevice, stream));
-  if (nU) PERM_CUDA_TRY(cudaMemcpyAsync(d + nv0, s.U.data(), nU * 8, cudaMemcpyHostToDevice, stream));
+  std::vector<int64_t> in(s.v0);
+  in.insert(in.end(), s.U.begin(), s.U.end());
+  char* base = nullptr;
+  size_t out_off = 0;
+  int st = int_stage(in.data(), in.size() * 8, blocks * 64, stream, &base, &out_off);
+  if (st) return st;
+  int64_t* d = reinterpret_cast<int64_t*>(base);
   IntWalkArgs a;
   a.v0 = d;
   a.U = d + nv0;
@@ -188,14 +212,12 @@ static int checked_range(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream
   a.wlen = 0;
   a.k_begin = k0;
   a.nchunks = nchunks;
-  a.out = d + nv0 + nU;
+  a.out = reinterpret_cast<int64_t*>(base + out_off);
   int_walk_checked_kernel<<<(unsigned)blocks, kIntThreads, 0, stream>>>(a);
   PERM_CUDA_TRY(cudaGetLastError());
   std::vector<int64_t> h(blocks * 8);
-  PERM_CUDA_TRY(cudaMemcpyAsync(h.data(), a.out, blocks * 64, cudaMemcpyDeviceToHost, stream));
-  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
-  PERM_CUDA_TRY(cudaFreeAsync(buf.p, stream));
-  buf.p = nullptr;
+  st = int_fetch(a.out, blocks * 64, stream, h.data());
+  if (st) return st;
   // ordered combine of block summaries (Gray order = block order); the
   // empty prefix (0) is included, as in the kernel's identity element
   s128 G = 0, mn = 0, mx = 0;
@@ -297,11 +319,11 @@ static int wrap_range_fp(const IntSetup& s, const FpGroups& g, uint64_t k0, uint
   for (int j = 0; j < P; ++j) buf[j] = (double)s.v0[g.order[j]];
   for (int t = 0; t < s.B; ++t)
     for (int j = 0; j < P; ++j) buf[P + (size_t)t * P + j] = (double)s.U[(size_t)t * P + g.order[j]];
-  const size_t bytes = buf.size() * 8 + blocks * 64 + 256;
-  DevBuf dbuf;
-  PERM_CUDA_TRY(cudaMallocAsync(&dbuf.p, bytes, stream));
-  double* d = static_cast<double*>(dbuf.p);
-  PERM_CUDA_TRY(cudaMemcpyAsync(d, buf.data(), buf.size() * 8, cudaMemcpyHostToDevice, stream));
+  char* base = nullptr;
+  size_t out_off = 0;
+  int st = int_stage(buf.data(), buf.size() * 8, blocks * 64, stream, &base, &out_off);
+  if (st) return st;
+  double* d = reinterpret_cast<double*>(base);
   IntWalkFArgs a;
   a.v0 = d;
   a.U = d + s.v0.size();
@@ -310,7 +332,7 @@ static int wrap_range_fp(const IntSetup& s, const FpGroups& g, uint64_t k0, uint
   a.log2L = log2L;
   a.k_begin = k0;
   a.nchunks = nchunks;
-  a.out = reinterpret_cast<int64_t*>(d + buf.size());
+  a.out = reinterpret_cast<int64_t*>(base + out_off);
   walk_fn_if fn = int_wrap_fp_lookup(s.P, g.ng);
   if (!fn) {
     set_error("no fp int walk for this size");
@@ -318,10 +340,8 @@ static int wrap_range_fp(const IntSetup& s, const FpGroups& g, uint64_t k0, uint
   }
   PERM_CUDA_TRY(fn(a, (int)blocks, stream));
   std::vector<int64_t> h(blocks * 8);
-  PERM_CUDA_TRY(cudaMemcpyAsync(h.data(), a.out, blocks * 64, cudaMemcpyDeviceToHost, stream));
-  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
-  PERM_CUDA_TRY(cudaFreeAsync(dbuf.p, stream));
-  dbuf.p = nullptr;
+  st = int_fetch(a.out, blocks * 64, stream, h.data());
+  if (st) return st;
   unsigned __int128 acc = 0;
   double H = 0, L = 0, M = 0;
   for (uint64_t b = 0; b < blocks; ++b) {
@@ -359,13 +379,14 @@ static int wrap_range(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream_t 
   const uint64_t nchunks = steps >> log2L;
   uint64_t blocks = std::min<uint64_t>((nchunks + kIntThreads - 1) / kIntThreads, (uint64_t)nsm * 8);
   const size_t nv0 = wide ? s.v0w.size() : s.v0.size(), nU = s.U.size(), nw = s.w.size();
-  const size_t bytes = (nv0 + nU + nw) * 8 + blocks * 16;
-  DevBuf buf;
-  PERM_CUDA_TRY(cudaMallocAsync(&buf.p, bytes, stream));
-  int64_t* d = static_cast<int64_t*>(buf.p);
-  PERM_CUDA_TRY(cudaMemcpyAsync(d, (wide ? s.v0w : s.v0).data(), nv0 * 8, cudaMemcpyHostToDevice, stream));
-  if (nU) PERM_CUDA_TRY(cudaMemcpyAsync(d + nv0, (wide ? s.R : s.U).data(), nU * 8, cudaMemcpyHostToDevice, stream));
-  if (nw) PERM_CUDA_TRY(cudaMemcpyAsync(d + nv0 + nU, s.w.data(), nw * 8, cudaMemcpyHostToDevice, stream));
+  std::vector<int64_t> in(wide ? s.v0w : s.v0);
+  in.insert(in.end(), (wide ? s.R : s.U).begin(), (wide ? s.R : s.U).end());
+  in.insert(in.end(), s.w.begin(), s.w.end());
+  char* base = nullptr;
+  size_t out_off = 0;
+  int st = int_stage(in.data(), in.size() * 8, blocks * 16, stream, &base, &out_off);
+  if (st) return st;
+  int64_t* d = reinterpret_cast<int64_t*>(base);
   IntWalkArgs a;
   a.v0 = d;
   a.U = d + nv0;
@@ -376,7 +397,7 @@ static int wrap_range(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream_t 
   a.wlen = (int)nw;
   a.k_begin = k0;
   a.nchunks = nchunks;
-  a.out = d + nv0 + nU + nw;
+  a.out = reinterpret_cast<int64_t*>(base + out_off);
   walk_fn_i fast = (g8 && log2L >= 3) ? int_wrap_lookup(s.P) : nullptr;
   if (fast) {
     PERM_CUDA_TRY(fast(a, (int)blocks, stream));
@@ -388,10 +409,8 @@ static int wrap_range(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream_t 
     PERM_CUDA_TRY(cudaGetLastError());
   }
   std::vector<int64_t> h(blocks * 2);
-  PERM_CUDA_TRY(cudaMemcpyAsync(h.data(), a.out, blocks * 16, cudaMemcpyDeviceToHost, stream));
-  PERM_CUDA_TRY(cudaStreamSynchronize(stream));
-  PERM_CUDA_TRY(cudaFreeAsync(buf.p, stream));
-  buf.p = nullptr;
+  st = int_fetch(a.out, blocks * 16, stream, h.data());
+  if (st) return st;
   unsigned __int128 acc = 0;
   for (uint64_t b = 0; b < blocks; ++b)
     acc += ((unsigned __int128)(uint64_t)h[2 * b + 1] << 64) | (uint64_t)h[2 * b];
