@@ -175,6 +175,50 @@ def check_value(n: int, v: float) -> dict:
     return {"value": v, "checked": True, "ref_ryser_dd": dd, "rel_err": rel, "scaled_err": scaled}
 
 
+def measure_configs(P, W, torch) -> dict:
+    """BASELINE configs[0..3] on one GPU: median wall clock of the public
+    call on host numpy input, device time for device-resident batches."""
+    def wall(fn, reps=5, warm=2):
+        for _ in range(warm):
+            fn()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts)
+
+    out = {}
+    c1 = W.c1()
+    out["C1_glynn_batch_64x12x12"] = {"e2e_ms": 1e3 * wall(lambda: P.glynn_batch(c1), reps=11)}
+    for name, A in (("C2a_opt_batch_1e6x8x8", W.c2a()), ("C2b_opt_batch_1e6x4x10", W.c2b())):
+        e2e = wall(lambda: P.opt_batch(A), reps=3, warm=1)
+        dA = torch.tensor(A, device="cuda")
+        P.opt_batch(dA)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            P.opt_batch(dA)
+        e1.record()
+        torch.cuda.synchronize()
+        dev_ms = e0.elapsed_time(e1) / 10
+        out[name] = {"e2e_ms": 1e3 * e2e, "device_ms": dev_ms, "hbm_gbs_device": A.nbytes / (dev_ms * 1e-3) / 1e9}
+        del dA
+    c3 = json.loads((ROOT / "tests" / "golden" / "c3.json").read_text())
+    for name, a, key in (("C3a_glynn_c128_24x24", W.c3a(), "c3a"), ("C3b_glynn_c128_20x28", W.c3b(), "c3b")):
+        v = P.glynn(a)
+        ref = complex(c3[f"{key}_dd_glynn"]["re"], c3[f"{key}_dd_glynn"]["im"])
+        out[name] = {"e2e_ms": 1e3 * wall(lambda: P.glynn(a)),
+                     "rel_err_vs_dd": abs(v - ref) / max(abs(v), abs(ref))}
+    c4 = json.loads((ROOT / "tests" / "golden" / "c4.json").read_text())
+    for name, a, key in (("C4a_glynn_int128_01_n32", W.c4a(), "c4a"), ("C4b_glynn_int128_pm2_n28", W.c4b(), "c4b")):
+        v = P.glynn(a, exact="int128")
+        out[name] = {"e2e_ms": 1e3 * wall(lambda: P.glynn(a, exact="int128"), reps=3, warm=1),
+                     "exact_matches_fixture": str(v) == str(c4[f"{key}_exact"])}
+    return out
+
+
 # ------------------------------------------------------------- engine arm
 def run_engine(args):
     # stdout carries the JSON line only: under torchrun, NCCL prints its
@@ -349,6 +393,14 @@ def _run_engine(args, json_fd):
                           ("steps_per_s" if alg == "glynn" else "subsets_per_s"): tot / (dms * 1e-3),
                           "frac_of_pipe": tot * 2 * ns / (dms * 1e-3) / peak_pipe}
 
+    # ---- the other BASELINE configs (rank 0, outside the timed region):
+    # public-API wall clock on host inputs (e2e) and, for the device-resident
+    # batches, the kernel's device time; each checked against its committed
+    # reference value where one exists (tests/golden)
+    configs = {}
+    if rank == 0 and not args.no_configs:
+        configs = measure_configs(P, W, torch)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
@@ -381,7 +433,8 @@ def _run_engine(args, json_fd):
                        "launch": {"grid": grid.value, "threads": 256, "log2_chunk": log2L.value},
                        "value_check": check,
                        "per_rank": per_rank,
-                       "n_sweep_1gpu": sweep},
+                       "n_sweep_1gpu": sweep,
+                       "configs_1gpu": configs},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_pipe, "unit": "FP64 op/s",
                          "frac": achieved / peak_pipe, "frac_of_fma_peak": achieved / peak_dfma,
                          "frac_of_nominal": achieved / NOMINAL_DFMA,
@@ -420,6 +473,7 @@ def main():
     ap.add_argument("--n", type=int, default=36)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1-C4 section (configs_1gpu)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.impl == "reference":
