@@ -211,10 +211,9 @@ void walk_exp(double* d_part, double* d_final, unsigned* d_done, double* d_data)
       t4max = std::max(t4max, t[4]);
       for (int k = 0; k < 4; ++k) ph[k] += (double)(t[k + 1] - t[k]) / plan.grid;
     }
-    double seed = 0;
-    printf("P=%d timeline%s (ns, grid %d): block start spread %llu | stage %.0f | seed+walk %.0f%.0f | block reduce %.0f | "
+    printf("P=%d timeline%s (ns, grid %d): block start spread %llu | stage %.0f | seed+walk %.0f | block reduce %.0f | "
            "combine %.0f (avg) | last t3 -> end %llu | span %llu\n",
-           P, "", plan.grid, t0max - t0min, ph[0], seed, ph[1], ph[2], ph[3], t4max - t3max,
+           P, "", plan.grid, t0max - t0min, ph[0], ph[1], ph[2], ph[3], t4max - t3max,
            t4max - t0min);
     unsigned long long* z = nullptr;
     cudaMemcpyToSymbol(g_walk_tl, &z, sizeof(z));
