@@ -370,8 +370,8 @@ def _run_engine(args, json_fd):
     # launch-to-launch gaps included), which frac_of_pipe is computed from
     sweep = {}
     if rank == 0:
-        for alg, ns in (("glynn", 20), ("glynn", 22), ("glynn", 24), ("glynn", 26), ("glynn", 28), ("glynn", 32),
-                        ("ryser", 24), ("ryser", 28), ("ryser", 32)):
+        for alg, ns in (("glynn", 20), ("glynn", 22), ("glynn", 24), ("glynn", 26), ("glynn", 28), ("glynn", 30),
+                        ("glynn", 32), ("glynn", 34), ("ryser", 24), ("ryser", 28), ("ryser", 32)):
             asw = np.ascontiguousarray(W.c5(ns))
             tot = (1 << (ns - 1)) if alg == "glynn" else (1 << ns)
             fn = P.glynn if alg == "glynn" else P.ryser
