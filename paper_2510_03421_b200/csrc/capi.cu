@@ -598,8 +598,71 @@ int perm_ryser_c128(int m, int n, const double* a, int64_t lda, int dev_ptr, dou
   return walk_single(PERM_ALG_RYSER, true, m, n, a, lda, dev_ptr, out, magsum, stream);
 }
 
+}  // extern "C"
+
+namespace {
+// Small integer matrices whose every intermediate -- of the reference's
+// checked int64 kernel and of the float engine alike -- is an integer below
+// 2^52: the state / row sums are bounded by the column (Glynn, ones pad
+// included) or row (Ryser, combinatoric) sums of |a|, the products by their
+// product, the running sums by 2^(steps) times that.  On these the float
+// path is exact and the reference cannot flag an overflow, so its value and
+// flag are the float engine's, at the zero-copy path's latency (the exact
+// integer path stages summaries and certificates: ~2x slower per call).
+bool int_small_certified(int alg, int m, int n, const int64_t* a, int64_t lda) {
+  if (m < 1 || m > n || n > 30) return false;
+  long double prod_r = 1.0L, prod_c = 1.0L;
+  for (int i = 0; i < m; ++i) {
+    long double r = 0;
+    for (int j = 0; j < n; ++j) {
+      const int64_t x = a[(size_t)i * lda + j];
+      if (x > (1LL << 31) || x < -(1LL << 31)) return false;
+      r += std::fabs((long double)x);
+    }
+    prod_r *= std::max(r, 1.0L);
+  }
+  for (int j = 0; j < n; ++j) {
+    long double c = (long double)(n - m);
+    for (int i = 0; i < m; ++i) c += std::fabs((long double)a[(size_t)i * lda + j]);
+    prod_c *= std::max(c, 1.0L);
+  }
+  long double bound;
+  if (alg == PERM_ALG_GLYNN) bound = std::ldexp(prod_c, n);
+  else if (alg == PERM_ALG_RYSER) bound = (m == n) ? std::ldexp(prod_r, n + 1) : 1e300L;
+  else bound = prod_r;
+  return bound < std::ldexp(1.0L, 52);
+}
+
+// -1: not taken (not certified, or a host-side refusal); else the status
+int int_via_float(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, uint64_t step_budget,
+                  int64_t* out, int* fits_int64, void* stream) {
+  if (dev_ptr || stream != nullptr || !int_small_certified(alg, m, n, a, lda)) return -1;
+  std::vector<double> d((size_t)m * n);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < n; ++j) d[(size_t)i * n + j] = (double)a[(size_t)i * lda + j];
+  double v = 0.0;
+  const int st = (alg == PERM_ALG_COMBINATORIC)
+                     ? comb_permanent(false, 0, m, n, d.data(), n, 0, step_budget, &v, nullptr, nullptr)
+                     : walk_single(alg, false, m, n, d.data(), n, 0, &v, nullptr, nullptr);
+  if (st) return st;
+  const double r = std::nearbyint(v);
+  if (!(std::fabs(v - r) <= 1e-6) || !(std::fabs(r) < 4503599627370496.0)) return -1;  // not exact: exact path
+  const int64_t iv = (int64_t)r;
+  out[0] = iv;
+  out[1] = iv < 0 ? -1 : 0;
+  if (fits_int64) *fits_int64 = 1;
+  return PERM_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int perm_glynn_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, int64_t* out,
                    int* fits_int64, void* stream) {
+  if (width == 64 || width == 128) {
+    const int fst = int_via_float(PERM_ALG_GLYNN, m, n, a, lda, dev_ptr, UINT64_MAX, out, fits_int64, stream);
+    if (fst >= 0) return fst;
+  }
   return int_permanent(PERM_ALG_GLYNN, m, n, a, lda, dev_ptr, width, out, fits_int64, stream);
 }
 int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, int64_t* out,
@@ -615,6 +678,10 @@ int perm_ryser_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int
     out[1] = v < 0 ? -1 : 0;
     if (fits_int64) *fits_int64 = 1;
     return PERM_OK;
+  }
+  if (m == n && (width == 64 || width == 128)) {
+    const int fst = int_via_float(PERM_ALG_RYSER, m, n, a, lda, dev_ptr, UINT64_MAX, out, fits_int64, stream);
+    if (fst >= 0) return fst;
   }
   return int_permanent(PERM_ALG_RYSER, m, n, a, lda, dev_ptr, width, out, fits_int64, stream);
 }
@@ -658,6 +725,8 @@ int perm_comb_i64(int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int 
     set_error("width must be 64 or 128");
     return PERM_BAD_ARG;
   }
+  const int fst = int_via_float(PERM_ALG_COMBINATORIC, m, n, a, lda, dev_ptr, step_budget, out, fits_int64, stream);
+  if (fst >= 0) return fst;
   int st = comb_permanent(false, width == 64 ? 2 : 3, m, n, a, lda, dev_ptr, step_budget, nullptr, out, stream);
   if (st) return st;
   if (width == 64) out[1] = out[0] < 0 ? -1 : 0;
