@@ -284,7 +284,38 @@ __global__ void __launch_bounds__(kCombThreads) comb_dfs_kernel(CombArgs A) {
   uint64_t p1 = p0 + A.per_thread;
   if (p1 > A.total) p1 = A.total;
   PERM_CHECK(D >= 1 && D <= m && m <= 64 && n <= kCombMaxN);
-  for (uint64_t pidx = p0; pidx < p1 && !sm.flag; ++pidx) {
+  // Whole permutations in the prefix (D == m, n <= 32; every single
+  // combinatoric of up to ~1e6 permutations): the used columns are a bit
+  // mask and the k-th free column is __fns -- no local-memory arrays, whose
+  // per-thread setup was most of a small call's 9 us kernel.  Same products
+  // in the same order, same zero pruning (src/_kernels.py:52).
+  const bool whole = !kInt && D == m && n <= 32;
+  if constexpr (!kInt) {
+  for (uint64_t pidx = p0; whole && pidx < p1; ++pidx) {
+    uint64_t rem = pidx, radix_prod = 1;
+    for (int q = 1; q < D; ++q) radix_prod *= (uint64_t)(n - q);
+    unsigned freem = (n == 32) ? 0xffffffffu : ((1u << n) - 1u);
+    T p = Num<T>::one();
+    bool pruned = false;
+    for (int q = 0; q < m; ++q) {
+      const uint64_t digit = rem / radix_prod;
+      rem -= digit * radix_prod;
+      if (q + 1 < D) radix_prod /= (uint64_t)(n - q - 1);
+      const int c = (int)__fns(freem, 0u, (int)digit + 1);
+      freem &= ~(1u << c);
+      p = Num<T>::mul(p, a[q * n + c]);
+      if (q < m - 1 && is_zero(p)) {
+        pruned = true;
+        break;
+      }
+    }
+    if (!pruned) {
+      dd_acc(hi, lo, Num<T>::re(p));
+      dd_acc(hi_i, lo_i, Num<T>::im(p));
+    }
+  }
+  }
+  for (uint64_t pidx = p0; !whole && pidx < p1 && !sm.flag; ++pidx) {
     // decode prefix: mixed radix (n, n-1, ..., n-D+1), most significant first
     int choice[64];
     bool used[kCombMaxN];

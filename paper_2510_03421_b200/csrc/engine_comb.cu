@@ -1,5 +1,6 @@
 // Host side of the combination-ordered Ryser and the combinatoric DFS.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "comb.cuh"
@@ -209,7 +210,11 @@ int comb_permanent(bool ryser, int mode, int m, int n, const void* a, int64_t ld
   // tiny float combinatoric from host memory: the zero-copy batch-of-one path
   // (memoized-DP kernel, m <= 4; the generic thread-per-matrix DFS is slower
   // than the tree-split comb kernel below from 5x5 on)
-  if (!ryser && mode <= 1 && !dev_ptr && lda == n && stream_ == nullptr && m <= 4 && n <= 12) {
+  static const int tiny_max_m = [] {  // PERM_TINY_COMB_MAX_M (measurement knob)
+    const char* e = std::getenv("PERM_TINY_COMB_MAX_M");
+    return (e && *e) ? std::atoi(e) : 4;
+  }();
+  if (!ryser && mode <= 1 && !dev_ptr && lda == n && stream_ == nullptr && m <= tiny_max_m && n <= 12) {
     const int tst = tiny_permanent(PERM_ALG_COMBINATORIC, mode == 1, m, n, static_cast<const double*>(a), out);
     if (tst >= 0) return tst;
   }
