@@ -7,8 +7,9 @@ The reference has no batch entry point -- ``as_matrix`` rejects anything but
 permanents with one kernel launch (C ABI perm_batch_*).  The batch dispatch
 (``opt_batch``) uses two batch-only exact formulas that are cheaper per
 matrix than any of the reference's algorithms: the set-partition (Moebius)
-formula for m <= 6 and the 4+4 Laplace expansion for 8x8, both streamed
-through shared memory by bulk copies (csrc/batch_bulk.cuh).
+formula for m <= 6 and, for 8x8, the row-by-row subset recursion with its
+middle level parked in tensor memory, both streamed through shared memory by
+bulk copies (csrc/batch_bulk.cuh).
 
 Integer batches return exact Python ints with the single-matrix semantics:
 matrices whose magnitudes certify exact FP64 arithmetic run on the batch
@@ -81,7 +82,7 @@ def _int_batch(arr, code):
 
     Matrices whose magnitudes certify that every intermediate of the batch
     formula is an integer below 2^52 run on the float batch kernels, where
-    FP64 is then exact: the partition / Laplace formulas need
+    FP64 is then exact: the partition / 8x8 row-recursion formulas need
     m! * prod_i (row sum of |a|) < 2^52 (every partial sum is a signed sum of
     permanent monomials of |A|, weighted by at most m! in total), square
     Glynn needs 2^(n-1) * prod_j (column sum of |a|) < 2^52.  Under the same
@@ -150,7 +151,9 @@ def partition_batch(a):
 
 
 def laplace_batch(a):
-    """8x8: sum_{|X|=4} per(A[0:4, X]) per(A[4:8, X^c])."""
+    """8x8 batch formula (the name is kept from round 1): the row-by-row
+    subset recursion f_L(S) = sum_{j in S} a_{L-1,j} f_{L-1}(S \\ {j}),
+    1016 FP64 ops per matrix (csrc/batch_bulk.cuh RowDp8Tm)."""
     return _run(a, "laplace")
 
 

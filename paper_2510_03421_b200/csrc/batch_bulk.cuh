@@ -27,13 +27,12 @@
 //    (2^m-1) adds per column = 26n + 30 flops (C2b: 290, against 3080 for the
 //    reference's cheapest exact algorithm, Ryser-rect).
 //    Thread per matrix.
-//  * Square 8x8 (C2a): generalised Laplace expansion over the 4+4 row split,
-//    per = sum_{|X|=4} per(A[0:4, X]) per(A[4:8, X^c]), with the 4x4 minors
-//    built from 2x2 row-pair permanents q(P):
-//      per(A[0:4, X]) = sum_{P subset X, |P|=2} q01(P) q23(X \ P).
-//    A thread owns one matrix: its 4 x 28 q-tables, the top half's 70 minors
-//    parked in shared memory, the bottom half's 70 minors on the complements.
-//    1134 flops per matrix against 2048 for Glynn.
+//  * Square 8x8 (C2a): the row-by-row subset recursion
+//    f_L(S) = sum_{j in S} a_{L-1,j} f_{L-1}(S \ {j}), per = f_8({0..7}),
+//    1016 flops per matrix against 2048 for Glynn; one thread per matrix,
+//    the middle level parked in tensor memory (perm8_tmem_kernel, RowDp8Tm).
+//    (The round-1 4+4 Laplace split, 1134 flops, now lives in
+//    tools/laplace8_variants.cuh as a measured alternative.)
 #pragma once
 #include <utility>
 #include "common.cuh"
@@ -402,150 +401,364 @@ __global__ void __launch_bounds__(128) partition_rt_kernel(const T* __restrict__
   out[i] = partition_combine<T, M>(S);
 }
 
-// ---------------------------------------------------- square 8x8: Laplace
-__host__ __device__ constexpr int lp_pidx(int i, int k) { return i * (15 - i) / 2 + (k - i - 1); }  // i < k < 8
-struct LpSub {
-  int x[4], c[4];
-};
-// the p-th 4-subset X of {0..7} containing column 0 (35 of them), and X^c
-__host__ __device__ constexpr LpSub lp_sub(int p) {
-  LpSub s{};
+// ---------------------------------------- TMEM as per-thread scratch (8x8)
+// A thread-per-matrix 8x8 kernel needs ~1.3 KB of scratch per matrix beyond
+// its registers.  In shared memory that scratch plus a 16 KB tile slot per
+// stage per warp held the round-1 kernel at 4 warps per SM (one per
+// scheduler, FP64 pipe ~60% busy on fixed-latency waits).  Here the scratch
+// lives in tensor memory: 256 KB per SM that nothing else on this path uses.
+// Lane i of warp w owns TMEM lane 32*(w%4)+i and 256 columns of it
+// (tcgen05.st / tcgen05.ld, 32x32b shape: one thread, consecutive 32-bit
+// columns).  A thread copies its whole matrix out of the tile at once (rows
+// 0..3 -> registers, rows 4..7 -> TMEM), so a warp releases its slot before
+// any arithmetic and one stage per warp keeps the copy of its next tile in
+// flight during the whole compute.  Shared memory is then just the tile ring,
+// 16 KB per warp: 8 warps per SM.
+__device__ __forceinline__ uint32_t tm_lo(double x) { return (uint32_t)__double2loint(x); }
+__device__ __forceinline__ uint32_t tm_hi(double x) { return (uint32_t)__double2hiint(x); }
+__device__ __forceinline__ double tm_pack(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
+#define TM_D2(d, i) "r"(tm_lo(d[i])), "r"(tm_hi(d[i]))
+// store D doubles (2D consecutive columns) of this thread's TMEM lane at column address ta
+__device__ __forceinline__ void tm_st8(uint32_t ta, const double* d) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      TM_D2(d, 0), TM_D2(d, 1), TM_D2(d, 2), TM_D2(d, 3), TM_D2(d, 4), TM_D2(d, 5), TM_D2(d, 6), TM_D2(d, 7)
+      : "memory");
+}
+__device__ __forceinline__ void tm_st4(uint32_t ta, const double* d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), TM_D2(d, 0),
+               TM_D2(d, 1), TM_D2(d, 2), TM_D2(d, 3)
+               : "memory");
+}
+__device__ __forceinline__ void tm_st2(uint32_t ta, const double* d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta), TM_D2(d, 0), TM_D2(d, 1)
+               : "memory");
+}
+#undef TM_D2
+__device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t (&r)[16]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+               : "r"(ta)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t ta, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(ta)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld4(uint32_t ta, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(ta)
+               : "memory");
+}
+// tcgen05.wait::ld, tied to the loaded registers so no use is scheduled above it
+__device__ __forceinline__ void tm_wait_ld(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Column map of a thread's TMEM lane (one CTA slice of kTmCols columns):
+// the parked level (70 doubles, 140 columns) from column 0, in groups of G
+// at 2G*k; rows 4..7 as two rotated 16-entry row-pair vectors at kTmRaw.
+constexpr int kTmCols = 256, kTmRaw = 144;
+
+// C doubles of this thread's TMEM lane from / to column ta: 8-double chunks, then 4, then 2
+template <int C>
+__device__ __forceinline__ void tm_st_n(uint32_t ta, const double* g) {
+#pragma unroll
+  for (int i = 0; i < C / 8; ++i) tm_st8(ta + 16 * i, g + 8 * i);
+  if constexpr (C % 8 >= 4) tm_st4(ta + 16 * (C / 8), g + 8 * (C / 8));
+  if constexpr (C % 4 >= 2) tm_st2(ta + 16 * (C / 8) + 8 * ((C % 8) / 4), g + 8 * (C / 8) + 4 * ((C % 8) / 4));
+  static_assert(C % 2 == 0, "pairs of minors");
+}
+template <int C>
+__device__ __forceinline__ void tm_ld_n(uint32_t ta, uint32_t (&r)[((2 * C + 15) / 16) * 16]) {
+  constexpr int F = C / 8;
+#pragma unroll
+  for (int i = 0; i < F; ++i) tm_ld16(ta + 16 * i, *reinterpret_cast<uint32_t(*)[16]>(r + 16 * i));
+  if constexpr (C % 8 != 0) {
+#pragma unroll
+    for (int i = 16 * F; i < 16 * F + 16; ++i) r[i] = 0u;
+    if constexpr (C % 8 >= 4) tm_ld8(ta + 16 * F, r + 16 * F);
+    if constexpr (C % 4 >= 2) tm_ld4(ta + 16 * F + 8 * ((C % 8) / 4), r + 16 * F + 8 * ((C % 8) / 4));
+  }
+}
+template <int NR>
+__device__ __forceinline__ void tm_wait_ld_n(uint32_t (&r)[NR]) {
+  tm_wait_ld(*reinterpret_cast<uint32_t(*)[16]>(r));
+#pragma unroll
+  for (int i = 1; i < NR / 16; ++i) {  // tie the other chunks behind the wait
+    uint32_t(&q)[16] = *reinterpret_cast<uint32_t(*)[16]>(r + 16 * i);
+    asm volatile(""
+                 : "+r"(q[0]), "+r"(q[1]), "+r"(q[2]), "+r"(q[3]), "+r"(q[4]), "+r"(q[5]), "+r"(q[6]), "+r"(q[7]),
+                   "+r"(q[8]), "+r"(q[9]), "+r"(q[10]), "+r"(q[11]), "+r"(q[12]), "+r"(q[13]), "+r"(q[14]), "+r"(q[15]));
+  }
+}
+// the rotated row pair (2p, 2p+1) of a lane's matrix as 16 doubles (row 2p^t in v[0..7])
+__device__ __forceinline__ void rd_pair(const double2* M, int p, int rho, int t, double (&v)[16]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double2 x = M[8 * p + ((((c & 3) + rho) & 3) | (((c >> 2) ^ t) << 2))];
+    v[(c >> 2) * 8 + 2 * (c & 3)] = x.x;
+    v[(c >> 2) * 8 + 2 * (c & 3) + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void tm_ld_pair(uint32_t ta, double (&v)[16]) {
+  uint32_t r0[16], r1[16];
+  tm_ld16(ta, r0);
+  tm_ld16(ta + 16, r1);
+  tm_wait_ld(r0);
+  tm_wait_ld(r1);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[i] = tm_pack(r0[2 * i], r0[2 * i + 1]);
+    v[8 + i] = tm_pack(r1[2 * i], r1[2 * i + 1]);
+  }
+}
+
+// ------------------------------------------ 8x8 row-by-row subset recursion
+// per(A) = f_8({0..7}) with f_1(S) = a_0j (S = {j}) and
+//   f_L(S) = sum_{j in S} a_{L-1,j} f_{L-1}(S \ {j})        (|S| = L),
+// the permanent of rows 0..L-1 on the columns S.  Level L costs L * C(8, L)
+// FP64 ops: 56 + 168 + 280 + 280 + 168 + 56 + 8 = 1016 per matrix for
+// levels 2..8, against 1134 for the 4+4 Laplace split (which pays 6 ops per
+// 4x4 minor on both halves).  Levels 2, 3 and 6..8 pull from the level below
+// in registers; level 4 (70 values) is parked in TMEM while level 5 is built
+// by pushing each parked value into the 56 level-5 accumulators (the first
+// push to an accumulator is a DMUL, the rest DFMAs), so neither level has to
+// be register-resident at the same time as its neighbour.  Subsets of size L
+// are ranked by increasing bit mask.
+__host__ __device__ constexpr int rd_popc(int m) { return m ? (m & 1) + rd_popc(m >> 1) : 0; }
+__host__ __device__ constexpr int rd_mask(int k, int r) {
   int q = 0;
-  for (int a = 1; a < 8; ++a)
-    for (int b = a + 1; b < 8; ++b)
-      for (int c = b + 1; c < 8; ++c) {
-        if (q == p) {
-          s.x[0] = 0; s.x[1] = a; s.x[2] = b; s.x[3] = c;
-          int k = 0;
-          for (int j = 1; j < 8; ++j)
-            if (j != a && j != b && j != c) s.c[k++] = j;
-        }
-        ++q;
-      }
-  return s;
+  for (int m = 0; m < 256; ++m)
+    if (rd_popc(m) == k) {
+      if (q == r) return m;
+      ++q;
+    }
+  return -1;
 }
-// per(H[:, {a,b,c,d}]) of a 4-row half H from its row-pair tables qa (rows
-// 0,1) and qb (rows 2,3) is the sum over the 6 ordered splits of {a,b,c,d}
-// into two pairs, qa(pair) * qb(other pair): one DMUL + five DFMAs.
-// Term s (0..5, the ordered splits (ab|cd) (cd|ab) (ac|bd) (bd|ac) (ad|bc)
-// (bc|ad)) of minor slot (pair, side) of the 35 (X, X^c) pairs: the index of
-// its qa (which = 0) or qb (which = 1) factor.
-__host__ __device__ constexpr int lp_term(int pair, int side, int s, int which) {
-  const LpSub q = lp_sub(pair);
-  const int a = side ? q.c[0] : q.x[0], b = side ? q.c[1] : q.x[1];
-  const int c = side ? q.c[2] : q.x[2], d = side ? q.c[3] : q.x[3];
-  // the 6 ordered splits: (ab|cd) (cd|ab) (ac|bd) (bd|ac) (ad|bc) (bc|ad)
-  const int p0[6][2] = {{a, b}, {c, d}, {a, c}, {b, d}, {a, d}, {b, c}};
-  const int p1[6][2] = {{c, d}, {a, b}, {b, d}, {a, c}, {b, c}, {a, d}};
-  return which == 0 ? lp_pidx(p0[s][0], p0[s][1]) : lp_pidx(p1[s][0], p1[s][1]);
+__host__ __device__ constexpr int rd_rank(int m) {
+  int q = 0;
+  for (int x = 0; x < m; ++x) q += rd_popc(x) == rd_popc(m);
+  return q;
 }
-// 2x2 row-pair permanents of the 8 logical columns held as 16 doubles (row r0 = v[0..7], r1 = v[8..15])
-__device__ __forceinline__ void lp_qtable(const double (&v)[16], double (&q)[28]) {
+__host__ __device__ constexpr int rd_bit(int m, int t) {  // t-th set bit of m (t-th clear bit: pass ~m & 255)
+  for (int j = 0; j < 8; ++j)
+    if ((m >> j) & 1) {
+      if (t == 0) return j;
+      --t;
+    }
+  return -1;
+}
+__host__ __device__ constexpr int rd_first_push(int m) {  // rank of the smallest-rank (|m|-1)-subset of m
+  int best = 1 << 20;
+  for (int j = 0; j < 8; ++j)
+    if ((m >> j) & 1) best = rd_rank(m & ~(1 << j)) < best ? rd_rank(m & ~(1 << j)) : best;
+  return best;
+}
+template <int L, int R, int T>
+constexpr int rd_col_v = rd_bit(rd_mask(L, R), T);  // column of term T of entry R of level L
+template <int L, int R, int T>
+constexpr int rd_src_v = rd_rank(rd_mask(L, R) & ~(1 << rd_bit(rd_mask(L, R), T)));  // its level L-1 entry
+// term T of level-L entries R0 + Ms (term-major: runs of independent DFMAs)
+template <int L, int R0, int T, int NS, int ND, int... Ms>
+__device__ __forceinline__ void rd_term(const double (&src)[NS], const double* row, double (&dst)[ND], int dofs,
+                                        std::integer_sequence<int, Ms...>) {
+  if constexpr (T == 0)
+    ((dst[dofs + Ms] = row[rd_col_v<L, R0 + Ms, 0>] * src[rd_src_v<L, R0 + Ms, 0>]), ...);
+  else
+    ((dst[dofs + Ms] = fma(row[rd_col_v<L, R0 + Ms, T>], src[rd_src_v<L, R0 + Ms, T>], dst[dofs + Ms])), ...);
+}
+template <int L, int R0, int NS, int ND, int... Ms, int... Ts>
+__device__ __forceinline__ void rd_pull(const double (&src)[NS], const double* row, double (&dst)[ND], int dofs,
+                                        std::integer_sequence<int, Ms...> ms, std::integer_sequence<int, Ts...>) {
+  (rd_term<L, R0, Ts>(src, row, dst, dofs, ms), ...);
+}
+// level L entries [R0, R0 + C) into dst[dofs ...]
+template <int L, int R0, int C, int NS, int ND>
+__device__ __forceinline__ void rd_level_part(const double (&src)[NS], const double* row, double (&dst)[ND], int dofs) {
+  rd_pull<L, R0>(src, row, dst, dofs, std::make_integer_sequence<int, C>{}, std::make_integer_sequence<int, L>{});
+}
+// level L (all C(8, L) entries) in groups of G
+template <int L, int G, int NS, int ND, int... Ks>
+__device__ __forceinline__ void rd_level(const double (&src)[NS], const double* row, double (&dst)[ND],
+                                         std::integer_sequence<int, Ks...>) {
+  ((rd_level_part<L, G * Ks, (ND - G * Ks < G ? ND - G * Ks : G)>(src, row, dst, G * Ks)), ...);
+}
+// level 4 group K (G entries) -> TMEM columns 2GK
+template <int G, int K>
+__device__ __forceinline__ void rd_l4_group(const double (&f3)[56], const double* r3, uint32_t tb) {
+  constexpr int C = (70 - G * K < G) ? 70 - G * K : G;
+  double g[C];
+  rd_level_part<4, G * K, C>(f3, r3, g, 0);
+  tm_st_n<C>(tb + 2 * G * K, g);
+}
+template <int G, int... Ks>
+__device__ __forceinline__ void rd_l4(const double (&f3)[56], const double* r3, uint32_t tb,
+                                      std::integer_sequence<int, Ks...>) {
+  (rd_l4_group<G, Ks>(f3, r3, tb), ...);
+}
+// push level-4 entry T = T0 + I/4 times a_4j (j its (I%4)-th missing column) into level 5
+template <int T0, int I>
+__device__ __forceinline__ void rd_push1(const double* x, const double* r4, double (&f5)[56]) {
+  constexpr int T = T0 + I / 4, MT = rd_mask(4, T), J = rd_bit(~MT & 255, I % 4), S = rd_rank(MT | (1 << J));
+  if constexpr (rd_first_push(MT | (1 << J)) == T) f5[S] = r4[J] * x[I / 4];
+  else f5[S] = fma(r4[J], x[I / 4], f5[S]);
+}
+template <int T0, int... Is>
+__device__ __forceinline__ void rd_push(const double* x, const double* r4, double (&f5)[56],
+                                        std::integer_sequence<int, Is...>) {
+  (rd_push1<T0, Is>(x, r4, f5), ...);
+}
+// level 5 from the parked level 4, G entries per TMEM load; group K+1's load
+// is issued before group K's pushes, so the TMEM latency hides behind them
+template <int G, int K>
+__device__ __forceinline__ void rd_l5_group(uint32_t tb, const double* r4, double (&f5)[56],
+                                            uint32_t (&cur)[((2 * G + 15) / 16) * 16]) {
+  constexpr int NG = (70 + G - 1) / G;
+  constexpr int C = (70 - G * K < G) ? 70 - G * K : G;
+  constexpr int NR = ((2 * G + 15) / 16) * 16;
+  tm_wait_ld_n(cur);
+  double x[C];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int k = i + 1; k < 8; ++k) q[lp_pidx(i, k)] = fma(v[i], v[8 + k], v[k] * v[8 + i]);
+  for (int i = 0; i < C; ++i) x[i] = tm_pack(cur[2 * i], cur[2 * i + 1]);
+  if constexpr (K + 1 < NG) {
+    constexpr int C1 = (70 - G * (K + 1) < G) ? 70 - G * (K + 1) : G;
+    static_assert(((2 * C1 + 15) / 16) * 16 <= NR, "");
+    tm_ld_n<C1>(tb + 2 * G * (K + 1), *reinterpret_cast<uint32_t(*)[((2 * C1 + 15) / 16) * 16]>(cur));
+  }
+  rd_push<G * K>(x, r4, f5, std::make_integer_sequence<int, 4 * C>{});
+}
+template <int G, int... Ks>
+__device__ __forceinline__ void rd_l5(uint32_t tb, const double* r4, double (&f5)[56],
+                                      std::integer_sequence<int, Ks...>) {
+  uint32_t cur[((2 * G + 15) / 16) * 16];
+  tm_ld_n<(G < 70 ? G : 70)>(tb, cur);
+  (rd_l5_group<G, Ks>(tb, r4, f5, cur), ...);
 }
 
-
-// Thread per matrix: the top half's 70 minors go to the thread's column of a
-// shared-memory buffer (conflict-free: consecutive threads, consecutive
-// words), then the bottom half's minors on the complements consume them --
-// no shuffles or selects.  Minors are built G at a time, term-major, so each
-// warp issues runs of G independent DFMAs.  The matrix is read with a
-// lane-dependent column rotation (pairs of columns, rho) and a swap of the
-// two rows of each 128-byte row (t): per is invariant under both, and every
-// LDS.128 of a warp is 4 wavefronts.
-template <int TPB, int G>
-struct Laplace8TOp {
-  static constexpr int kLanes = 1;
-  // term T of minor slot X (X = 2*pair + side; FLIP: the complement's minor)
-  template <int T, int FLIP, int X0, int... Ms>
-  __device__ __forceinline__ static void term(const double (&qa)[28], const double (&qb)[28], double (&g)[sizeof...(Ms)],
-                                              std::integer_sequence<int, Ms...>) {
-    if constexpr (T == 0) {
-      ((g[Ms] = qa[lp_term((X0 + Ms) >> 1, ((X0 + Ms) & 1) ^ FLIP, 0, 0)] *
-                qb[lp_term((X0 + Ms) >> 1, ((X0 + Ms) & 1) ^ FLIP, 0, 1)]),
-       ...);
-    } else {
-      ((g[Ms] = fma(qa[lp_term((X0 + Ms) >> 1, ((X0 + Ms) & 1) ^ FLIP, T, 0)],
-                    qb[lp_term((X0 + Ms) >> 1, ((X0 + Ms) & 1) ^ FLIP, T, 1)], g[Ms])),
-       ...);
-    }
-  }
-  template <int FLIP, int X0, int... Ms>
-  __device__ __forceinline__ static void minors(const double (&qa)[28], const double (&qb)[28],
-                                                double (&g)[sizeof...(Ms)], std::integer_sequence<int, Ms...> seq) {
-    term<0, FLIP, X0>(qa, qb, g, seq);
-    term<1, FLIP, X0>(qa, qb, g, seq);
-    term<2, FLIP, X0>(qa, qb, g, seq);
-    term<3, FLIP, X0>(qa, qb, g, seq);
-    term<4, FLIP, X0>(qa, qb, g, seq);
-    term<5, FLIP, X0>(qa, qb, g, seq);
-  }
-  template <int X0, int... Ms>
-  __device__ __forceinline__ static void minors_store(const double (&qa)[28], const double (&qb)[28], double* gcol,
-                                                      std::integer_sequence<int, Ms...> seq) {
-    double g[sizeof...(Ms)];
-    minors<0, X0>(qa, qb, g, seq);
-    ((gcol[(X0 + Ms) * TPB] = g[Ms]), ...);
-  }
-  template <int X0, int... Ms>
-  __device__ __forceinline__ static void minors_use(const double (&qc)[28], const double (&qd)[28], const double* gcol,
-                                                    double (&acc)[8], std::integer_sequence<int, Ms...> seq) {
-    double h[sizeof...(Ms)];
-    minors<1, X0>(qc, qd, h, seq);
-    ((acc[Ms & 7] = fma(gcol[(X0 + Ms) * TPB], h[Ms], acc[Ms & 7])), ...);
-  }
-  template <int... Ks>
-  __device__ __forceinline__ static void all_store(const double (&qa)[28], const double (&qb)[28], double* gcol,
-                                                   std::integer_sequence<int, Ks...>) {
-    (minors_store<Ks * G>(qa, qb, gcol, std::make_integer_sequence<int, (70 - Ks * G < G) ? 70 - Ks * G : G>{}), ...);
-  }
-  template <int... Ks>
-  __device__ __forceinline__ static void all_use(const double (&qc)[28], const double (&qd)[28], const double* gcol,
-                                                 double (&acc)[8], std::integer_sequence<int, Ks...>) {
-    (minors_use<Ks * G>(qc, qd, gcol, acc, std::make_integer_sequence<int, (70 - Ks * G < G) ? 70 - Ks * G : G>{}),
-     ...);
-  }
-  __device__ __forceinline__ static void load_q(const double2* H, int rho, int t, double (&q)[28]) {
-    double v[16];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const double2 x = H[(((c & 3) + rho) & 3) | (((c >> 2) ^ t) << 2)];
-      v[(c >> 2) * 8 + 2 * (c & 3)] = x.x;
-      v[(c >> 2) * 8 + 2 * (c & 3) + 1] = x.y;
-    }
-    lp_qtable(v, q);
-  }
+template <int G>
+struct RowDp8Tm {
+  static_assert(G % 2 == 0 && 2 * 70 <= kTmRaw, "level-4 groups fit below the raw block");
   template <class R>
-  __device__ __forceinline__ static void run(const double* tile, int64_t first, int cnt, double* out, int me,
-                                             R&& release) {
-    __shared__ double gbuf[70 * TPB];
-    const int lane = me & 31;
-    const int rho = lane & 3, t = (lane >> 2) & 1;
-    const double2* M = reinterpret_cast<const double2*>(tile + (size_t)me * 64);
-    double* gcol = gbuf + me;
-    {
-      double qa[28], qb[28];
-      load_q(M, rho, t, qa);
-      load_q(M + 8, rho, t, qb);
-      all_store(qa, qb, gcol, std::make_integer_sequence<int, (70 + G - 1) / G>{});
+  __device__ __forceinline__ static double run(const double2* M, int rho, int t, uint32_t tb, R&& release) {
+    double v01[16], v23[16];
+    rd_pair(M, 0, rho, t, v01);
+    rd_pair(M, 1, rho, t, v23);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // rows 4..7 wait in TMEM
+      double v[16];
+      rd_pair(M, 2 + h, rho, t, v);
+      tm_st8(tb + kTmRaw + 32 * h, v);
+      tm_st8(tb + kTmRaw + 32 * h + 16, v + 8);
     }
-    double qc[28], qd[28];
-    load_q(M + 16, rho, t, qc);
-    load_q(M + 24, rho, t, qd);
     release();
-    double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    all_use(qc, qd, gcol, acc, std::make_integer_sequence<int, (70 + G - 1) / G>{});
-    const double r = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-    if (me < cnt) out[first + me] = r;
+    double f3[56];
+    {
+      double f1[8], f2[28];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f1[j] = v01[j];
+      rd_level<2, 28>(f1, v01 + 8, f2, std::make_integer_sequence<int, 1>{});
+      rd_level<3, 14>(f2, v23, f3, std::make_integer_sequence<int, 4>{});
+    }
+    rd_l4<G>(f3, v23 + 8, tb, std::make_integer_sequence<int, (70 + G - 1) / G>{});
+    tm_wait_st();
+    double v45[16], v67[16];
+    tm_ld_pair(tb + kTmRaw, v45);
+    double f5[56];
+    rd_l5<G>(tb, v45, f5, std::make_integer_sequence<int, (70 + G - 1) / G>{});
+    tm_ld_pair(tb + kTmRaw + 32, v67);
+    double f6[28], f7[8];
+    rd_level<6, 14>(f5, v45 + 8, f6, std::make_integer_sequence<int, 2>{});
+    rd_level<7, 8>(f6, v67, f7, std::make_integer_sequence<int, 1>{});
+    // level 8 as two 4-term chains
+    double e0 = v67[8] * f7[rd_rank(255 & ~1)], e1 = v67[12] * f7[rd_rank(255 & ~16)];
+#pragma unroll
+    for (int j = 1; j < 4; ++j) {
+      e0 = fma(v67[8 + j], f7[7 - j], e0);
+      e1 = fma(v67[12 + j], f7[3 - j], e1);
+    }
+    return e0 + e1;
   }
 };
 
-  // 4 steps = 16 minors per group
-
-// 32 threads (matrices) per block, 7 minors per group: C2a 0.115 ms
-using Laplace8Op = Laplace8TOp<32, 7>;
+// One CTA of WARPS warps per TMEM slice: per-warp single-stage tile rings
+// (lane 0 arms the warp's mbarrier and issues its bulk copies), each thread
+// one matrix, Body::run calls release() once the lane's matrix is out of the
+// slot (registers + TMEM), so the warp's next tile streams in during the
+// arithmetic.
+template <int WARPS, class Body, bool kComputeOnly = false>
+__global__ void __launch_bounds__(32 * WARPS, 8 / WARPS) perm8_tmem_kernel(const double* __restrict__ a,
+                                                                           double* __restrict__ out, int64_t nb) {
+  static_assert(WARPS == 4 || WARPS == 8, "4 warps (two CTAs per SM) or 8 (one CTA) share the 512 TMEM columns");
+  constexpr unsigned TILE_BYTES = 32 * 64 * sizeof(double);
+  extern __shared__ __align__(128) unsigned char bb_smem_raw[];
+  __shared__ __align__(8) uint64_t full[WARPS];
+  __shared__ uint32_t tmem_base_sh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(bb_smem(&tmem_base_sh)),
+                 "n"(kTmCols * WARPS / 4)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  unsigned char* ring = bb_smem_raw + (size_t)warp * TILE_BYTES;
+  uint64_t* bar = &full[warp];
+  const int64_t ntiles = (nb + 31) / 32;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp, nw = (int64_t)gridDim.x * WARPS;
+  auto issue = [&](int64_t tile) {
+    const int64_t first = tile * 32;
+    const int64_t cnt = (nb - first < 32) ? nb - first : 32;
+    const unsigned bytes = (unsigned)cnt * 512u;
+    bb_expect_tx(bar, bytes);
+    bb_bulk_g2s(ring, reinterpret_cast<const char*>(a) + first * 512, bytes, bar);
+  };
+  if (lane == 0) {
+    bb_mbar_init(bar, 1);
+    bb_fence_mbar_init();
+    if (gw < ntiles) issue(gw);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tb = tmem_base_sh + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kTmCols);
+  const int rho = lane & 3, t = (lane >> 2) & 1;
+  unsigned phase = 0;
+  for (int64_t tile = gw; tile < ntiles; tile += nw) {
+    if (!kComputeOnly || tile == gw) bb_wait(bar, phase);  // (kComputeOnly: timing experiments)
+    phase ^= 1u;
+    const int64_t first = tile * 32;
+    const int cnt = (int)((nb - first < 32) ? nb - first : 32);
+    PERM_CHECK(cnt >= 1 && cnt <= 32 && first + cnt <= nb);
+    const double2* M = reinterpret_cast<const double2*>(ring + (size_t)lane * 512);
+    const double res = Body::run(M, rho, t, tb, [&]() {
+      __syncwarp();  // every lane holds its matrix: the slot is free
+      if (lane == 0) {
+        const int64_t nt = tile + nw;
+        if (nt < ntiles && !kComputeOnly) {
+          bb_fence_proxy_async();
+          issue(nt);
+        }
+      }
+    });
+    if (lane < cnt) out[first + lane] = res;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_sh),
+                 "n"(kTmCols * WARPS / 4)
+                 : "memory");
+  }
+}
 
 }  // namespace permb200

@@ -1,5 +1,5 @@
 // Host side of the bulk-pipelined batch kernels (batch_bulk.cuh): the
-// partition-formula kernel for m <= 6 and the 4+4 Laplace kernel for 8x8,
+// partition-formula kernel for m <= 6 and the 8x8 row-recursion kernel,
 // picked by the batch dispatch (perm_batch_select) for device-resident
 // batches that meet the 1-D bulk-copy rules (16-byte aligned base, matrix
 // size a multiple of 16 bytes).
@@ -61,24 +61,24 @@ cudaError_t launch_partition(const void* a, void* out, int64_t B, cudaStream_t s
   return cudaGetLastError();
 }
 
-// Laplace 8x8: 32 threads (matrices) per block, two stages, four blocks per
-// SM (240 registers, 18 KB of minors per block; C2a 1e6 x 8x8: 0.115 ms
-// against 0.184 ms for the thread-per-matrix Glynn kernel and 0.124 ms for a
-// lane-pair variant with shuffles, tools/bulk_bench.cu).
-constexpr int kLapTPB = 32, kLapStages = 2, kLapPerSM = 4;
+// 8x8: the row-by-row subset recursion with its middle level parked in TMEM
+// (RowDp8Tm), one 8-warp CTA per SM, each warp a single-stage 16 KB tile ring
+// (128 KB of shared memory, so one CTA per SM and its 512 TMEM columns).
+// C2a 1e6 x 8x8: 0.089 ms, 5.8 TB/s (round 1: 0.115 ms with the shared-memory
+// 4+4 Laplace kernel; tools/bulk_bench.cu).
+constexpr int kDp8Warps = 8;
 cudaError_t launch_laplace8(const void* a, void* out, int64_t B, cudaStream_t s) {
-  auto k = batch_bulk_kernel<double, 8, 8, kLapTPB, kLapStages, Laplace8Op>;
-  constexpr int kMats = kLapTPB / Laplace8Op::kLanes;
-  const size_t smem = (size_t)kLapStages * kMats * 64 * sizeof(double);
+  auto k = perm8_tmem_kernel<kDp8Warps, RowDp8Tm<8>>;
+  const size_t smem = (size_t)kDp8Warps * 32 * 64 * sizeof(double);
   static bool attr[16] = {false};
   if (!attr[cur_device()]) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr[cur_device()] = true;
   }
-  const int64_t ntiles = (B + kMats - 1) / kMats;
-  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)kLapPerSM * sm_count());
-  k<<<grid, kLapTPB, smem, s>>>(static_cast<const double*>(a), static_cast<double*>(out), B);
+  const int64_t ntiles = (B + 31) / 32;
+  const int grid = (int)std::min<int64_t>((ntiles + kDp8Warps - 1) / kDp8Warps, (int64_t)sm_count());
+  k<<<grid, 32 * kDp8Warps, smem, s>>>(static_cast<const double*>(a), static_cast<double*>(out), B);
   return cudaGetLastError();
 }
 

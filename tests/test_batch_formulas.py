@@ -6,7 +6,11 @@ checked against the oracle's restatement of the reference kernels (CPU):
   mu(pi) = prod_b (-1)^(|b|-1) (|b|-1)!  -- Moebius inversion from "maps
   constant on blocks" to injective maps (the reference's combinatoric sum,
   src/_kernels.py:28-56, reorganised).
-* Laplace (8x8): per(A) = sum_{|X|=4} per(A[0:4, X]) per(A[4:8, X^c]), the
+* row recursion (8x8, the engine's C2a kernel RowDp8Tm):
+  f_L(S) = sum_{j in S} a_{L-1,j} f_{L-1}(S \\ {j}), per(A) = f_8({0..7}),
+  with level 5 built by pushing the parked level 4 (first push a product).
+* Laplace (8x8, the round-1 kernel, kept in tools/laplace8_variants.cuh):
+  per(A) = sum_{|X|=4} per(A[0:4, X]) per(A[4:8, X^c]), the
   4x4 minors from 2x2 row-pair permanents q(P):
   per(H[:, X]) = sum_{P subset X, |P| = 2} q01(P) q23(X \\ P).
 
@@ -64,6 +68,42 @@ def laplace8(a):
     return tot
 
 
+def rowdp8(a):
+    """The kernel's evaluation order: levels 2-4 and 6-8 pull, level 5 pushes
+    level-4 entries in rank order (subsets ranked by increasing bit mask)."""
+    n = a.shape[0]
+    masks = {k: [m for m in range(1 << n) if bin(m).count("1") == k] for k in range(n + 1)}
+    f = {1 << j: a[0, j] for j in range(n)}
+    for L in range(2, n + 1):
+        g = {}
+        if L == 5:
+            for T in masks[4]:
+                for j in range(n):
+                    if not (T >> j) & 1:
+                        S = T | (1 << j)
+                        g[S] = a[4, j] * f[T] if S not in g else g[S] + a[4, j] * f[T]
+        else:
+            for S in masks[L]:
+                js = [j for j in range(n) if (S >> j) & 1]
+                g[S] = sum(a[L - 1, j] * f[S & ~(1 << j)] for j in js)
+        f = g
+    return f[(1 << n) - 1]
+
+
+def test_rowdp8_vs_oracle():
+    rng = np.random.default_rng(18)
+    for _ in range(3):
+        ai = rng.integers(-2, 3, (8, 8)).astype(np.int64)
+        assert rowdp8(ai) == O.permanent("glynn", ai)[0]  # exact on integers
+    assert rowdp8(np.ones((8, 8))) == 40320.0
+    assert rowdp8(np.eye(8)) == 1.0
+    af = rng.standard_normal((8, 8)) / np.sqrt(8)
+    ref = O.permanent("glynn", af)[0]
+    assert abs(rowdp8(af) - ref) <= 1e-12 * O.glynn_magnitude_sum(af)
+    # FP64 ops of the recursion, levels 2..8 (the kernel's 769 DFMA + 247 DMUL)
+    assert sum(L * math.comb(8, L) for L in range(2, 9)) == 1016
+
+
 def test_set_partition_counts():
     assert [sum(1 for _ in set_partitions(list(range(k)))) for k in range(1, 7)] == [1, 2, 5, 15, 52, 203]
     # |mu| summed over partitions of an m-set = m! (permutations by cycle type)
@@ -111,6 +151,7 @@ def test_kernel_symmetries():
             if t:
                 b = b[[1, 0, 3, 2, 5, 4, 7, 6]]
             assert abs(laplace8(b) - ref) <= 1e-12 * max(1.0, abs(ref))
+            assert abs(rowdp8(b) - ref) <= 1e-12 * max(1.0, abs(ref))
     r = rng.standard_normal((4, 10))
     for tau in range(4):
         assert abs(partition_formula(np.roll(r, -tau, axis=0)) - partition_formula(r)) <= 1e-12

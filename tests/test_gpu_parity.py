@@ -426,7 +426,7 @@ def test_partition_batch_all_shapes(cplx):
 
 
 def test_laplace_batch_8x8():
-    """The bulk-pipelined 4+4 Laplace kernel (C2a's batch dispatch) vs the
+    """The bulk-pipelined 8x8 row-recursion kernel (C2a's batch dispatch) vs the
     oracle; exact on small-integer matrices; complex 8x8 falls back to Glynn."""
     torch = pytest.importorskip("torch")
     rng = np.random.default_rng(88)

@@ -8,6 +8,7 @@
 #include <vector>
 #include "../paper_2510_03421_b200/csrc/batch.cuh"
 #include "../paper_2510_03421_b200/csrc/batch_bulk.cuh"
+#include "laplace8_variants.cuh"
 using namespace permb200;
 
 // streaming ceiling of the bulk pipeline: no arithmetic, one store per matrix
@@ -89,6 +90,25 @@ void run_warp(const char* name, const double* dA, double* dOut, int64_t B, int n
          B * (M * N * 8.0 + 8) / (ms * 1e-3) / 1e9, maxerr(h, ref, scale), cudaGetErrorString(e));
 }
 
+template <int WARPS, bool CO = false, int G = 8, class Body = Laplace8Tm<G>>
+void run_tmem(const char* name, const double* dA, double* dOut, int64_t B, int nsm, int per_sm, size_t smem_pad,
+              const std::vector<double>& ref, const std::vector<double>& scale) {
+  size_t smem = (size_t)WARPS * 32 * 512;
+  if (smem < smem_pad) smem = smem_pad;
+  auto k = perm8_tmem_kernel<WARPS, Body, CO>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { printf("%s smem %zu: %s\n", name, smem, cudaGetErrorString(e)); cudaGetLastError(); return; }
+  const int64_t ntiles = (B + 31) / 32;
+  const int grid = (int)std::min<int64_t>((ntiles + WARPS - 1) / WARPS, (int64_t)nsm * per_sm);
+  cudaMemset(dOut, 0, B * 8);
+  float ms = timeit([&] { k<<<grid, 32 * WARPS, smem>>>(dA, dOut, B); }, 20);
+  e = cudaGetLastError();
+  std::vector<double> h(B);
+  cudaMemcpy(h.data(), dOut, B * 8, cudaMemcpyDeviceToHost);
+  printf("%-10s TMEM W=%d grid=%4d smem=%6zu: %.4f ms  %.0f GB/s  err=%.2e %s\n", name, WARPS, grid, smem, ms,
+         B * (64 * 8.0 + 8) / (ms * 1e-3) / 1e9, maxerr(h, ref, scale), cudaGetErrorString(e));
+}
+
 int main() {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -119,6 +139,26 @@ int main() {
       scale[i] = p * 40320.0 / 16777216.0;  // ~ per(|A|)
     }
     printf("classic glynn 8x8: %.4f ms  %.0f GB/s\n", ms, B * 520.0 / (ms * 1e-3) / 1e9);
+    run_bulk<8, 8, 32, 2, Laplace8TOp<32, 7>>("lap8T g7", a, out, B, nsm, 4, ref, scale);
+    run_tmem<4>("lapTM 4x2", a, out, B, nsm, 2, 80 * 1024, ref, scale);
+    run_tmem<8>("lapTM 8x1", a, out, B, nsm, 1, 0, ref, scale);
+    run_tmem<8, true>("CO TM 8x1", a, out, B, nsm, 1, 0, ref, scale);
+    run_tmem<4, true>("CO TM 4x2", a, out, B, nsm, 2, 80 * 1024, ref, scale);
+    run_tmem<8, false, 8, RowDp8Tm<8>>("DP g8", a, out, B, nsm, 1, 0, ref, scale);
+    run_tmem<8, false, 16, RowDp8Tm<16>>("DP g16", a, out, B, nsm, 1, 0, ref, scale);
+    run_tmem<8, true, 8, RowDp8Tm<8>>("CO DP g8", a, out, B, nsm, 1, 0, ref, scale);
+    run_tmem<4, false, 8, RowDp8Tm<8>>("DP 4x2", a, out, B, nsm, 2, 80 * 1024, ref, scale);
+    {
+      const int64_t b3 = 999997;  // ragged last tile
+      run_tmem<8, false, 8, RowDp8Tm<8>>("DP rag", a, out, b3, nsm, 1, 0, std::vector<double>(ref.begin(), ref.begin() + b3),
+                  std::vector<double>(scale.begin(), scale.begin() + b3));
+    }
+    run_tmem<4>("lapTM 4x2", a, out, B, nsm, 2, 80 * 1024, ref, scale);
+    {
+      const int64_t b3 = 999997;  // ragged last tile
+      run_tmem<4>("lapTM rag", a, out, b3, nsm, 2, 80 * 1024, std::vector<double>(ref.begin(), ref.begin() + b3),
+                  std::vector<double>(scale.begin(), scale.begin() + b3));
+    }
     run_bulk<8, 8, 32, 2, Laplace8TOp<32, 10>>("lap8T 32", a, out, B, nsm, 4, ref, scale);
     run_bulk<8, 8, 32, 1, Laplace8TOp<32, 10>>("lap8T s1", a, out, B, nsm, 6, ref, scale);
     run_bulk<8, 8, 32, 1, Laplace8TOp<32, 10>>("lap8T s1", a, out, B, nsm, 7, ref, scale);

@@ -1,4 +1,4 @@
-"""All 1e6 matrices of C2a / C2b: the batch-only formulas (Laplace 8x8,
+"""All 1e6 matrices of C2a / C2b: the batch-only formulas (row recursion 8x8,
 set partitions 4x10) against the classic per-matrix kernels (Glynn /
 memoized combinatoric), with the error scaled by per(|A|) (the permanent's
 own magnitude sum, computed with the same kernels on |A|, where nothing
