@@ -2,10 +2,13 @@
 // (reference int64 semantics) and WRAP (certified int128) Gray walks.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <utility>
 
 #include "engine.cuh"
 #include "int_walk.cuh"
+#include "int_walk32.cuh"
 
 namespace permb200 {
 
@@ -180,7 +183,7 @@ struct IntPart {
   // (raw-sum units) with its magnitude sum for the fit certificate
   unsigned __int128 raw = 0;
   double est_hi = 0, est_lo = 0, mag = 0;
-  int est_kind = 0;  // 0 none, 1 fused FP64-exact walk, 2 separate float walk
+  int est_kind = 0;  // 0 none, 1 fused FP64-exact walk, 2 separate float walk, 3 fused FP32-quad walk (FP32 estimate), 4 FP32-quad walk with FP64 upper levels
   bool refused = false;  // entries too large for the FP64 certificate
 };
 
@@ -362,6 +365,147 @@ static int wrap_range_fp(const IntSetup& s, const FpGroups& g, uint64_t k0, uint
   return PERM_OK;
 }
 
+// FP32-quad path (int_walk32.cuh): the P state entries (padded with constant
+// ones to 4 NQ) are cut into NQ quads whose products of per-entry bounds stay
+// below 2^23, so state, pair and quad products are exact in FP32 and each
+// |quad| is a 23-bit integer.  Same longest-processing-time assignment as
+// int_fp_groups; `pos` maps the kernel's entry positions (oct-interleaved,
+// Walk32) to original state indices, -1 for a pad.
+constexpr int kQuadBoundLog2 = 23;
+struct F32Quads {
+  int nq = 0;
+  std::vector<int> pos;
+  int scale_log2 = 0;  // the estimate product carries 2^-scale_log2
+  // FP64 upper levels: every product of four consecutive quads' bounds is
+  // below 2^84 (dmul96 in int_walk32.cuh)
+  bool dl4 = false;
+};
+static bool int_f32_quads(const IntSetup& s, F32Quads* out) {
+  const int P = s.P;
+  if ((int)s.cb.size() != P || P < 1 || P > 4 * kInt32MaxQuads) return false;
+  const int NQ = (P + 3) / 4;
+  std::vector<int> idx(P);
+  for (int j = 0; j < P; ++j) idx[j] = j;
+  std::sort(idx.begin(), idx.end(), [&](int x, int y) { return s.cb[x] > s.cb[y]; });
+  std::vector<std::vector<int>> quad(NQ);
+  std::vector<long double> lg(NQ, 0.0L);
+  long double total = 0.0L;
+  for (int j : idx) {
+    if (s.cb[j] >= ((s128)1 << kQuadBoundLog2)) return false;
+    int best = -1;
+    for (int q = 0; q < NQ; ++q)
+      if (quad[q].size() < 4 && (best < 0 || lg[q] < lg[best])) best = q;
+    quad[best].push_back(j);
+    const long double l = std::log2((long double)(s.cb[j] < 1 ? (s128)1 : s.cb[j]));
+    lg[best] += l;
+    total += l;
+  }
+  for (int q = 0; q < NQ; ++q) {
+    uint64_t prod = 1;  // < 2^23 * 2^23 at every step
+    for (int j : quad[q]) {
+      prod *= (uint64_t)(s.cb[j] < 1 ? (s128)1 : s.cb[j]);
+      if (prod >= (1ull << kQuadBoundLog2)) return false;
+    }
+  }
+  // dmul96 multiplies quads [0, 4) (NQ >= 3) and quads [4, 8) (NQ >= 7)
+  out->dl4 = true;
+  for (int q0 = 0; q0 < 8; q0 += 4) {
+    if (NQ < q0 + 3) break;
+    unsigned __int128 prod = 1;  // four quads: < 2^92
+    for (int q = q0; q < std::min(NQ, q0 + 4); ++q)
+      for (int j : quad[q]) prod *= (unsigned __int128)(uint64_t)(s.cb[j] < 1 ? (s128)1 : s.cb[j]);
+    if (prod >= ((unsigned __int128)1 << 84)) out->dl4 = false;
+  }
+  // the FP32 product of all quads must stay a normal float: 2^-scale keeps it
+  // below 2^100, and the smallest nonzero |term| (>= 1) above 2^-120
+  const int scale = std::max(0, (int)std::ceil(total) - 100);
+  if (scale > 120) return false;
+  out->nq = NQ;
+  out->scale_log2 = scale;
+  out->pos.assign((size_t)4 * NQ, -1);
+  const int full = 2 * (NQ / 2);  // quads living in full octs
+  for (int q = 0; q < NQ; ++q)
+    for (size_t i = 0; i < quad[q].size(); ++i) {
+      const int at = q < full ? 8 * (q / 2) + 2 * (int)i + (q & 1) : 8 * (NQ / 2) + (int)i;
+      out->pos[at] = quad[q][i];
+    }
+  return true;
+}
+
+static bool f32_walk_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PERM_INT_F32");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+static bool f32_walk_ok(const IntSetup& s, uint64_t k0, uint64_t k1, F32Quads* g) {
+  return f32_walk_enabled() && !s.weighted && s.B >= 8 && s.B <= 62 && k1 - k0 >= 8 && range_align(k0, k1) >= 3 &&
+         int_f32_quads(s, g);
+}
+
+static int wrap_range_f32(const IntSetup& s, const F32Quads& g, uint64_t k0, uint64_t k1, cudaStream_t stream,
+                          IntPart* p) {
+  const uint64_t steps = k1 - k0;
+  const int amax = range_align(k0, k1);
+  int dev = 0, nsm = 148, resident = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  walk_fn_i32 fn = int_wrap_f32_lookup(g.nq, g.dl4, &resident);
+  if (!fn) {
+    set_error("no FP32-quad int walk for this size");
+    return PERM_BAD_SHAPE;
+  }
+  const uint64_t max_blocks = (uint64_t)nsm * resident;
+  const uint64_t lanes = max_blocks * kInt32Threads;
+  int log2L = 3;
+  while (log2L < 14 && log2L < amax && (steps >> (log2L + 1)) >= 16 * lanes) ++log2L;
+  const uint64_t nchunks = steps >> log2L;
+  const uint64_t blocks = std::min<uint64_t>((nchunks + kInt32Threads - 1) / kInt32Threads, max_blocks);
+  const int P4 = 4 * g.nq;
+  std::vector<float> buf((size_t)(s.B + 1) * P4);
+  for (int j = 0; j < P4; ++j) buf[j] = g.pos[j] < 0 ? 1.0f : (float)s.v0[g.pos[j]];
+  for (int t = 0; t < s.B; ++t)
+    for (int j = 0; j < P4; ++j)
+      buf[(size_t)(t + 1) * P4 + j] = g.pos[j] < 0 ? 0.0f : (float)s.U[(size_t)t * s.P + g.pos[j]];
+  char* base = nullptr;
+  size_t out_off = 0;
+  int st = int_stage(buf.data(), buf.size() * sizeof(float), blocks * 64, stream, &base, &out_off);
+  if (st) return st;
+  IntWalk32Args a;
+  a.v0 = reinterpret_cast<const float*>(base);
+  a.U = a.v0 + P4;
+  a.B = s.B;
+  a.log2L = log2L;
+  a.escale = std::ldexp(1.0f, -g.scale_log2);
+  a.k_begin = k0;
+  a.nchunks = nchunks;
+  a.out = reinterpret_cast<int64_t*>(base + out_off);
+  PERM_CUDA_TRY(fn(a, (int)blocks, stream));
+  std::vector<int64_t> h(blocks * 8);
+  st = int_fetch(a.out, blocks * 64, stream, h.data());
+  if (st) return st;
+  unsigned __int128 acc = 0;
+  double H = 0, L = 0, M = 0;
+  for (uint64_t b = 0; b < blocks; ++b) {
+    const int64_t* o = &h[b * 8];
+    acc += ((unsigned __int128)(uint64_t)o[1] << 64) | (uint64_t)o[0];
+    double hh, ll, mm;
+    std::memcpy(&hh, &o[2], 8);
+    std::memcpy(&ll, &o[3], 8);
+    std::memcpy(&mm, &o[4], 8);
+    dd_add(H, L, hh, ll);
+    M += mm;
+  }
+  p->raw = acc;
+  const int sc = g.dl4 ? 0 : g.scale_log2;  // the FP64 estimate is unscaled
+  p->est_hi = std::ldexp(H, sc);
+  p->est_lo = std::ldexp(L, sc);
+  p->mag = std::ldexp(M, sc);
+  p->est_kind = g.dl4 ? 4 : 3;
+  return PERM_OK;
+}
+
 static int wrap_range(const IntSetup& s, uint64_t k0, uint64_t k1, cudaStream_t stream, IntPart* p) {
   if (k1 == k0) return PERM_OK;
   const bool wide = s.bound >= ((s128)1 << 62);  // int64 state could wrap
@@ -489,8 +633,12 @@ static int plan_int(int alg, int m, int n, const int64_t* a, int64_t lda, int de
 }
 
 static long double est_error(const IntPart& p, int P) {
-  const long double c = p.est_kind == 1 ? (3 + (1 << 14) + 16) : (P + (1 << 14) + 16);
-  return c * std::ldexp(1.0L, -52) * (long double)p.mag;
+  // kind 4: FP64 product of <= 5 exact pair products (4 roundings)
+  const long double c = p.est_kind == 2 ? (P + (1 << 14) + 16) : ((p.est_kind == 4 ? 4 : 3) + (1 << 14) + 16);
+  // kind 3: each term's estimate is an FP32 product of exact quads (at most
+  // 6 roundings, relative error < 2^-21 of |term| <= |estimate| / (1 - 2^-21))
+  const long double f32 = p.est_kind == 3 ? std::ldexp(1.0L, -20) : 0.0L;
+  return (c * std::ldexp(1.0L, -52) + f32) * (long double)p.mag;
 }
 
 // One range.  `full` (the whole walk on one device) lets the separate float
@@ -499,6 +647,17 @@ static int int_part(int alg, const IntPlan& pl, int width, uint64_t k0, uint64_t
                     IntPart* p) {
   const IntSetup& s = pl.s;
   if (width == 64) return checked_range(s, k0, k1, stream, p);
+  F32Quads gq;
+  if (f32_walk_ok(s, k0, k1, &gq)) {
+    int st = wrap_range_f32(s, gq, k0, k1, stream, p);
+    if (st) return st;
+    // the FP32 estimate's certificate is looser than the FP64-exact walk's:
+    // when it cannot certify the fit on its own, take the FP64 paths below
+    if (!full || pl.cert_apriori ||
+        (long double)std::fabs(p->est_hi) + est_error(*p, s.P) < std::ldexp(1.0L, 126))
+      return PERM_OK;
+    *p = IntPart();
+  }
   FpGroups g;
   if (fp_walk_ok(s, k0, k1, &g)) return wrap_range_fp(s, g, k0, k1, stream, p);
   if (!pl.cert_apriori) {
