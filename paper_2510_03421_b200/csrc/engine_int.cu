@@ -377,7 +377,7 @@ struct F32Quads {
   std::vector<int> pos;
   int scale_log2 = 0;  // the estimate product carries 2^-scale_log2
   // FP64 upper levels: every product of four consecutive quads' bounds is
-  // below 2^84 (dmul96 in int_walk32.cuh)
+  // below 2^83 (dmul96s / dmul96 in int_walk32.cuh)
   bool dl4 = false;
 };
 static bool int_f32_quads(const IntSetup& s, F32Quads* out) {
@@ -414,7 +414,7 @@ static bool int_f32_quads(const IntSetup& s, F32Quads* out) {
     unsigned __int128 prod = 1;  // four quads: < 2^92
     for (int q = q0; q < std::min(NQ, q0 + 4); ++q)
       for (int j : quad[q]) prod *= (unsigned __int128)(uint64_t)(s.cb[j] < 1 ? (s128)1 : s.cb[j]);
-    if (prod >= ((unsigned __int128)1 << 84)) out->dl4 = false;
+    if (prod >= ((unsigned __int128)1 << 83)) out->dl4 = false;
   }
   // the FP32 product of all quads must stay a normal float: 2^-scale keeps it
   // below 2^100, and the smallest nonzero |term| (>= 1) above 2^-120

@@ -168,7 +168,7 @@ __device__ __forceinline__ u128w term_mag(const uint32_t (&q)[NQ]) {
 // into the 128-bit add (x ^ m) + (m & 1)
 __device__ __forceinline__ void acc_signed(uint32_t (&acc)[4], const u128w& p, uint32_t m) {
   const uint32_t x0 = p.w0 ^ m, x1 = p.w1 ^ m, x2 = p.w2 ^ m, x3 = p.w3 ^ m;
-  uint32_t scratch;
+  [[maybe_unused]] uint32_t scratch;
   // m + m carries out exactly when m = 0xffffffff: the +1 of the negation
   asm("add.cc.u32 %4, %9, %9;\n\t"
       "addc.cc.u32 %0, %0, %5;\n\t"
@@ -183,59 +183,112 @@ __device__ __forceinline__ void acc_signed(uint32_t (&acc)[4], const u128w& p, u
 // The FP64 pipe is idle in this walk, while the 32x32 -> 64 integer multiplies
 // of the upper product levels saturate the heavy FMA pipe (ncu: IMAD.WIDE is
 // 4 cycles there).  With the quads converted to double, a pair of quads
-// r = q q' < 2^46 is one exact DMUL, and the product of two such r (< 2^84,
-// certified by the host) comes out of three more FP64 operations as an exact
-// (high, low) split at 2^32:
-//   t  = fma(|a|, |b|, 2^84)        mantissa of t = H = round(|a b| / 2^32)
-//   e  = fma(|a|, |b|, -(t - 2^84))  exact remainder, |e| <= 2^31
-// so |a b| = H 2^32 + e, assembled into three words with three integer adds.
+// r = q q' (|r| < 2^46) is one exact DMUL, and the product of two such r
+// (|a b| < 2^83, certified by the host) comes out of three more FP64
+// operations as an exact (high, low) split at 2^32, rounding DOWN:
+//   t  = fma_rd(a, b, 1.5 2^84)      mantissa of t = 2^51 + H, H = floor(a b / 2^32)
+//   e  = fma(a, b, -(t - 1.5 2^84))  exact remainder, 0 <= e < 2^32
+// so a b = H 2^32 + e with H in two's complement: the words of the signed
+// 128-bit product need one integer subtract and one shift.  The term's sign
+// (the other pair products' signs and the (-1)^k of the step) is moved into
+// `a` beforehand, so the 128-bit accumulate is a plain add.
+struct s128w {
+  uint32_t w0, w1, w2, w3;  // two's complement, w3 = sign extension of w2
+};
+template <bool NEG>
+__device__ __forceinline__ s128w dmul96s(double a, double b) {
+  const double M = 0x1.8p84;
+  const double t = NEG ? __fma_rd(-a, b, M) : __fma_rd(a, b, M);
+  const double ph = __dadd_rn(t, -M);
+  const double e = NEG ? __fma_rn(-a, b, -ph) : __fma_rn(a, b, -ph);
+  const long long eb = __double_as_longlong(__dadd_rn(e, 0x1p52));
+  const long long tb = __double_as_longlong(t);
+  s128w r;
+  r.w0 = (uint32_t)eb;
+  r.w1 = (uint32_t)tb;
+  r.w2 = (uint32_t)(tb >> 32) - 0x45380000u;
+  r.w3 = (uint32_t)((int32_t)r.w2 >> 31);
+  return r;
+}
+// |a b| < 2^84 as three words (unsigned operand of the last product)
 __device__ __forceinline__ u96 dmul96(double a, double b) {
   const double M = 0x1p84;
   const double aa = fabs(a), bb = fabs(b);
-  const double t = __fma_rn(aa, bb, M);
+  const double t = __fma_rd(aa, bb, M);
   const double ph = __dadd_rn(t, -M);
   const double e = __fma_rn(aa, bb, -ph);
-  const long long eb = __double_as_longlong(__dadd_rn(e, 0x1.8p52));
-  const uint32_t b32 = (uint32_t)(eb >> 32) - 0x43380000u;  // 0, or 0xffffffff when e < 0
-  const uint64_t H = (uint64_t)__double_as_longlong(t) - 0x4530000000000000ull + (((uint64_t)b32 << 32) | b32);
+  const long long eb = __double_as_longlong(__dadd_rn(e, 0x1p52));
+  const long long tb = __double_as_longlong(t);
   u96 r;
   r.w0 = (uint32_t)eb;
-  r.w1 = lo32(H);
-  r.w2 = hi32(H);
+  r.w1 = (uint32_t)tb;
+  r.w2 = (uint32_t)(tb >> 32) - 0x45300000u;
   return r;
 }
 // |x| < 2^46, an exact integer -> uint64
 __device__ __forceinline__ uint64_t dmag48(double x) {
   return (uint64_t)__double_as_longlong(__dadd_rn(fabs(x), 0x1p52)) & 0xfffffffffffffull;
 }
+// x with its sign flipped when s is negative
+__device__ __forceinline__ double flip_sign(double x, double s) {
+  const int hi = __double2hiint(x) ^ (__double2hiint(s) & (int)0x80000000);
+  return __hiloint2double(hi, __double2loint(x));
+}
+// (A B) mod 2^128 for a signed A (two's complement, |A| < 2^96) and B < 2^96:
+// mul96 on A's words plus the sign word's product (-B 2^96 when A < 0)
+__device__ __forceinline__ u128w mul96s(const s128w& A, const u96& B) {
+  u96 a;
+  a.w0 = A.w0; a.w1 = A.w1; a.w2 = A.w2;
+  u128w c = mul96(a, B);
+  c.w3 = A.w3 * B.w0 + c.w3;
+  return c;
+}
 
-// |term| mod 2^128 from the quads as doubles; f = the FP64 product of the
-// pair products (the term's estimate and sign)
-template <int NQ>
-__device__ __forceinline__ u128w term_mag_d(const double (&qd)[NQ], double& f) {
+// The signed term (-1)^NEG prod(quads) mod 2^128 from the quads as doubles;
+// f = the FP64 product of the pair products (the term's estimate, unsigned by NEG)
+template <int NQ, bool NEG>
+__device__ __forceinline__ u128w term_signed_d(const double (&qd)[NQ], double& f) {
   constexpr int NR = (NQ + 1) / 2;
   double r[NR];
 #pragma unroll
   for (int i = 0; i < NQ / 2; ++i) r[i] = __dmul_rn(qd[2 * i], qd[2 * i + 1]);
   if constexpr (NQ & 1) r[NR - 1] = qd[NQ - 1];
+  u128w p;
   if constexpr (NR == 1) {
     f = r[0];
-    return widen(widen48(dmag48(r[0])));
+    const long long x = NEG ? -__double2ll_rn(r[0]) : __double2ll_rn(r[0]);
+    p.w0 = (uint32_t)x; p.w1 = (uint32_t)(x >> 32); p.w2 = p.w3 = (uint32_t)(x >> 63);
   } else if constexpr (NR == 2) {
     f = __dmul_rn(r[0], r[1]);
-    return widen(dmul96(r[0], r[1]));
-  } else if constexpr (NR == 3) {
-    f = __dmul_rn(__dmul_rn(r[0], r[1]), r[2]);
-    return mul128x48(widen(dmul96(r[0], r[1])), dmag48(r[2]));
+    const s128w A = dmul96s<NEG>(r[0], r[1]);
+    p.w0 = A.w0; p.w1 = A.w1; p.w2 = A.w2; p.w3 = A.w3;
   } else {
-    f = __dmul_rn(__dmul_rn(r[0], r[1]), __dmul_rn(r[2], r[3]));
-    u128w p = mul96(dmul96(r[0], r[1]), dmul96(r[2], r[3]));
-    if constexpr (NR == 5) {
-      f = __dmul_rn(f, r[4]);
-      p = mul128x48(p, dmag48(r[4]));
+    // rest = the product of the other pair products: its sign moves into r[0]
+    double rest;
+    if constexpr (NR == 3) rest = r[2];
+    if constexpr (NR == 4) rest = __dmul_rn(r[2], r[3]);
+    if constexpr (NR == 5) rest = __dmul_rn(__dmul_rn(r[2], r[3]), r[4]);
+    f = __dmul_rn(__dmul_rn(r[0], r[1]), rest);
+    const s128w A = dmul96s<NEG>(flip_sign(r[0], rest), r[1]);
+    if constexpr (NR == 3) {
+      u128w a;
+      a.w0 = A.w0; a.w1 = A.w1; a.w2 = A.w2; a.w3 = A.w3;
+      p = mul128x48(a, dmag48(r[2]));
+    } else {
+      p = mul96s(A, dmul96(r[2], r[3]));
+      if constexpr (NR == 5) p = mul128x48(p, dmag48(r[4]));
     }
-    return p;
   }
+  return p;
+}
+
+__device__ __forceinline__ void acc_add(uint32_t (&acc)[4], const u128w& p) {
+  asm("add.cc.u32 %0, %0, %4;\n\t"
+      "addc.cc.u32 %1, %1, %5;\n\t"
+      "addc.cc.u32 %2, %2, %6;\n\t"
+      "addc.u32 %3, %3, %7;"
+      : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3])
+      : "r"(p.w0), "r"(p.w1), "r"(p.w2), "r"(p.w3));
 }
 
 // State: NQ quads = 2 NQ packed pairs.  Full octs (8 entries, 4 packed regs
@@ -309,14 +362,15 @@ struct Walk32 {
 #pragma unroll
       for (int i = 0; i < NQ; ++i) qd[i] = (double)qf[i];
       double d;
-      const u128w p = term_mag_d<NQ>(qd, d);
-      uint32_t m = (uint32_t)(__double2hiint(d) >> 31);
-      if (neg) m = ~m;
-      acc_signed(acc, p, m);
-      est = neg ? est - d : est + d;
+      if (neg) {
+        acc_add(acc, term_signed_d<NQ, true>(qd, d));
+        est -= d;
+      } else {
+        acc_add(acc, term_signed_d<NQ, false>(qd, d));
+        est += d;
+      }
       mag += fabs(d);
-      return;
-    }
+    } else {
     f32x2 e;  // packed running product of the quad pairs (estimate)
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
@@ -352,6 +406,7 @@ struct Walk32 {
     const double d = (double)f;
     est = neg ? est - d : est + d;
     mag += fabs(d);
+    }
   }
 };
 
