@@ -214,7 +214,15 @@ def measure_configs(P, W, torch) -> dict:
     c4 = json.loads((ROOT / "tests" / "golden" / "c4.json").read_text())
     for name, a, key in (("C4a_glynn_int128_01_n32", W.c4a(), "c4a"), ("C4b_glynn_int128_pm2_n28", W.c4b(), "c4b")):
         v = P.glynn(a, exact="int128")
-        out[name] = {"e2e_ms": 1e3 * wall(lambda: P.glynn(a, exact="int128"), reps=3, warm=1),
+        t = wall(lambda: P.glynn(a, exact="int128"), reps=3, warm=1)
+        # which exact walk ran (report the pipe): the est_kind
+        # slot of the width-128 partial, 3 / 4 = the quad walk (packed FP32
+        # state, FP64 pair products, integer last level), 1 = FP64-exact groups
+        from paper_2510_03421_b200 import sharded as S
+        kind = int(S.gpu_partial_int("glynn", a, 0, 1 << (a.shape[1] - 1), exact="int128")[5])
+        out[name] = {"e2e_ms": 1e3 * t, "steps_per_s": (1 << (a.shape[1] - 1)) / t,
+                     "walk": {4: "quad walk: FP32x2 + FP64 + IMAD pipes", 3: "quad walk: FP32x2 + IMAD pipes",
+                              1: "FP64-exact groups + IMAD"}.get(kind, f"est_kind {kind}"),
                      "exact_matches_fixture": str(v) == str(c4[f"{key}_exact"])}
     return out
 
@@ -392,6 +400,26 @@ def _run_engine(args, json_fd):
             sweep[key] = {"call_ms": 1e3 * statistics.median(walls), "device_ms": dms,
                           ("steps_per_s" if alg == "glynn" else "subsets_per_s"): tot / (dms * 1e-3),
                           "frac_of_pipe": tot * 2 * ns / (dms * 1e-3) / peak_pipe}
+            if alg == "glynn" and ns <= 26:
+                # throughput of the same size through the batch entry point (B
+                # independent matrices of the same law, device resident, one
+                # segmented walk launch): what a caller with many n x n
+                # permanents gets; a single small permanent is launch-latency bound
+                Bn = 1 << (29 - ns)
+                rb = np.random.default_rng([2510, 3421, 10 + ns, 1])
+                dA = torch.tensor(rb.uniform(0, 1, (Bn, ns, ns)) / ns, device="cuda")
+                P.glynn_batch(dA)
+                torch.cuda.synchronize()
+                b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                b0.record()
+                for _ in range(5):
+                    P.glynn_batch(dA)
+                b1.record()
+                torch.cuda.synchronize()
+                bms = b0.elapsed_time(b1) / 5
+                sweep[key].update({"batch_B": Bn, "batch_ms": bms, "batch_steps_per_s": Bn * tot / (bms * 1e-3),
+                                   "batch_frac_of_pipe": Bn * tot * 2 * ns / (bms * 1e-3) / peak_pipe})
+                del dA
 
     # ---- the other BASELINE configs (rank 0, outside the timed region):
     # public-API wall clock on host inputs (e2e) and, for the device-resident

@@ -627,7 +627,12 @@ bool int_small_certified(int alg, int m, int n, const int64_t* a, int64_t lda) {
     prod_c *= std::max(c, 1.0L);
   }
   long double bound;
-  if (alg == PERM_ALG_GLYNN) bound = std::ldexp(prod_c, n);
+  // Glynn: square only.  The rectangular float walk runs on the pre-scaled
+  // matrix 2^s A (build_walk); with s < 0 its state entries are multiples of
+  // 2^s and the n-factor products need up to n |s| more mantissa bits, so
+  // they are not exact (found by the int128 fuzz: a 7x9 matrix with one
+  // column of 674s came back 84 off).
+  if (alg == PERM_ALG_GLYNN) bound = (m == n) ? std::ldexp(prod_c, n) : 1e300L;
   else if (alg == PERM_ALG_RYSER) bound = (m == n) ? std::ldexp(prod_r, n + 1) : 1e300L;
   else bound = prod_r;
   return bound < std::ldexp(1.0L, 52);

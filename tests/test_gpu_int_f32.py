@@ -10,6 +10,7 @@ FP64-exact walk of int_walk.cuh)."""
 from __future__ import annotations
 
 import json
+import math
 import os
 import subprocess
 import sys
@@ -113,3 +114,68 @@ def test_sharded_ranges_sum_to_the_whole():
         parts = [S.gpu_partial_int(alg, a, *S.shard_range(alg, m, n, r, 3), exact="int128") for r in range(3)]
         assert {int(p[5]) for p in parts} <= {3, 4}
         assert S.finish_int(alg, a, np.stack(parts), exact="int128") == want
+
+
+def test_int128_fuzz():
+    """Seeded fuzz of the exact int128 entry points over shapes 9 <= n <= 22
+    (square and rectangular Glynn, square Ryser), 0/1 densities and signed
+    entry ranges on both sides of the quad walk's eligibility bounds, against
+    the oracle's exact integers.  PERM_FUZZ_INT128 cases (default 80)."""
+    rng = np.random.default_rng(20261022)
+    kinds = {}
+    for case in range(int(os.environ.get("PERM_FUZZ_INT128", "80"))):
+        n = int(rng.integers(9, 23))
+        m = n if case % 3 else int(rng.integers(max(2, n - 6), n + 1))
+        law = case % 5
+        if law == 0:
+            a = (rng.random((m, n)) < rng.uniform(0.2, 0.9)).astype(np.int64)
+        elif law == 1:
+            k = int(rng.integers(1, 4))
+            a = rng.integers(-k, k + 1, (m, n)).astype(np.int64)
+        elif law == 2:
+            k = int(rng.integers(4, 13))
+            a = rng.integers(-k, k + 1, (m, n)).astype(np.int64)
+        elif law == 3:
+            a = ((rng.random((m, n)) < 0.3) * rng.integers(-40, 41, (m, n))).astype(np.int64)
+        else:
+            a = rng.integers(0, 3, (m, n)).astype(np.int64)
+            a[:, int(rng.integers(0, n))] *= int(rng.integers(1, 2000))  # one heavy column
+        # the oracle's int128 walks wrap silently: Ryser's raw sum is the
+        # permanent itself, so it is the reference value (|per| < 2^127 here)
+        want = O.exact_int128("ryser", a)
+        for alg in ("glynn",) + (("ryser",) if m == n else ()):
+            try:
+                got = getattr(P, alg)(a, exact="int128")
+            except OverflowError:
+                # allowed only when the walk's raw sum (value x 2^(n-1) (n-m)!
+                # for Glynn) is past the certified range |raw| < 2^126
+                raw = abs(want) * ((1 << (n - 1)) * math.factorial(n - m) if alg == "glynn" else 1)
+                assert raw >= 1 << 126, (case, alg, m, n, want)
+                continue
+            assert got == want, (case, alg, m, n, law)
+            k = est_kind(alg, a) if m == n else -1
+            kinds[k] = kinds.get(k, 0) + 1
+    assert kinds.get(4, 0) > 0 and kinds.get(3, 0) + kinds.get(1, 0) + kinds.get(2, 0) + kinds.get(0, 0) > 0, kinds
+
+
+def test_rectangular_glynn_small_integers_stay_exact():
+    """Regression (found by the fuzz above): a small rectangular integer matrix
+    with one heavy column once took the certified float route, whose power-of-
+    two pre-scale makes the rectangular Glynn products inexact (84 off)."""
+    a = np.array([[2, 0, 0, 0, 2, 0, 0, 674, 0], [0, 2, 0, 1, 2, 2, 2, 0, 2], [2, 1, 2, 1, 2, 1, 1, 674, 1],
+                  [0, 0, 0, 0, 1, 1, 0, 674, 1], [2, 2, 2, 2, 1, 0, 1, 337, 1], [1, 2, 0, 2, 0, 0, 0, 0, 2],
+                  [2, 1, 1, 0, 2, 0, 0, 337, 2]], dtype=np.int64)
+    want = O.permanent("combinatoric", a)[0]
+    assert want == 32535348
+    assert P.glynn(a, exact="int128") == want
+    assert P.glynn(a) == want and P.ryser(a) == want and P.combinatoric(a) == want and P.opt(a) == want
+    rng = np.random.default_rng(77)
+    for _ in range(40):  # small rectangular integer matrices, default (checked) and int128
+        n = int(rng.integers(3, 11))
+        m = int(rng.integers(1, n))
+        b = rng.integers(0, 3, (m, n)).astype(np.int64)
+        b[:, int(rng.integers(0, n))] *= int(rng.integers(1, 3000))
+        ref, ovf = O.permanent("glynn", b)
+        if not ovf:
+            assert P.glynn(b) == ref, b
+        assert P.glynn(b, exact="int128") == O.exact_int128("ryser", b), b
