@@ -1,0 +1,104 @@
+"""Seeded fuzz with harsh value laws (heavy columns and rows, wide dynamic
+range, exact zeros, integer-valued floats, near-singular structure) through
+every single-matrix entry point, float and integer, against the CPU oracle.
+Needs a B200.
+
+Float: metric (ii) <= 1e-10 with M = the larger of the oracle's Glynn and
+Ryser magnitude sums.  Integer: bit-exact values and the
+reference's OverflowError on exactly the same inputs.
+PERM_FUZZ_HARSH cases (default 120)."""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_2510_03421_b200 as P
+from conftest import scaled_err
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def harsh(rng, m, n, law):
+    a = rng.uniform(-1, 1, (m, n))
+    if law == 0:  # one heavy column
+        a[:, rng.integers(0, n)] *= 10.0 ** rng.uniform(1, 6)
+    elif law == 1:  # row scales over 2^+-20
+        a *= (2.0 ** rng.uniform(-20, 20, (m, 1)))
+    elif law == 2:  # column scales over 2^+-12
+        a *= (2.0 ** rng.uniform(-12, 12, (1, n)))
+    elif law == 3:  # sparse with exact zeros, a zero column now and then
+        a *= rng.random((m, n)) < 0.35
+        if rng.random() < 0.3:
+            a[:, rng.integers(0, n)] = 0.0
+    elif law == 4:  # integer-valued floats
+        a = np.rint(a * rng.integers(1, 50)).astype(np.float64)
+    elif law == 5:  # nearly rank one (massive cancellation in Ryser)
+        a = np.outer(rng.uniform(0.5, 1.5, m), rng.uniform(0.5, 1.5, n)) + 1e-6 * a
+    elif law == 6:  # tiny and huge magnitudes together
+        a *= 10.0 ** rng.integers(-6, 7, (m, n))
+    else:  # all positive, close to the ones matrix
+        a = 1.0 + 1e-3 * a
+    return a
+
+
+def magsum2(a):
+    return max(O.glynn_magnitude_sum(a), O.ryser_magnitude_sum(a, nthreads=1))
+
+
+def test_harsh_float_laws():
+    rng = np.random.default_rng(20261023)
+    for case in range(int(os.environ.get("PERM_FUZZ_HARSH", "120"))):
+        n = int(rng.integers(2, 17))
+        m = int(rng.integers(1, n + 1)) if case % 2 else n
+        a = harsh(rng, m, n, case % 8)
+        if case % 5 == 4:
+            a = a + 1j * harsh(rng, m, n, (case // 8) % 8)
+        ref = O.dd_permanent("ryser" if m < n else "glynn", a, nthreads=4)
+        M = magsum2(a)
+        fns = [P.opt, P.glynn, P.ryser] + ([P.combinatoric] if math.perm(n, m) <= 500_000 else [])
+        for fn in fns:
+            got = fn(a)
+            assert scaled_err(got, ref, M) <= TOL, (case, fn.__name__, m, n, case % 8, got, ref, M)
+
+
+def test_harsh_integer_laws():
+    rng = np.random.default_rng(20261024)
+    for case in range(int(os.environ.get("PERM_FUZZ_HARSH", "120"))):
+        n = int(rng.integers(2, 13))
+        m = int(rng.integers(1, n + 1)) if case % 2 else n
+        law = case % 4
+        if law == 0:
+            a = rng.integers(0, 3, (m, n))
+            a[:, rng.integers(0, n)] *= int(rng.integers(1, 5000))
+        elif law == 1:
+            a = rng.integers(-3, 4, (m, n))
+            a[rng.integers(0, m), :] *= int(rng.integers(1, 5000))
+        elif law == 2:
+            a = rng.integers(-50, 51, (m, n)) * (rng.random((m, n)) < 0.5)
+        else:
+            a = rng.integers(-1, 2, (m, n)) * int(10 ** rng.integers(0, 5))
+        a = a.astype(np.int64)
+        algs = ["glynn", "ryser"] + (["combinatoric"] if math.perm(n, m) <= 500_000 else [])
+        for alg in algs:
+            want, ovf = O.permanent(alg, a)
+            fn = getattr(P, alg)
+            if ovf:
+                with pytest.raises(OverflowError):
+                    fn(a)
+            else:
+                assert fn(a) == want, (case, alg, m, n, law)
+        exact = O.exact_int128("ryser", a)
+        if abs(exact) < 1 << 90:
+            for alg in algs:
+                try:
+                    got = getattr(P, alg)(a, exact="int128")
+                except OverflowError:
+                    # Glynn's raw sum carries 2^(n-1) (n-m)!: refusals only past the certified range
+                    assert alg == "glynn" and abs(exact) * (1 << (n - 1)) * math.factorial(n - m) >= 1 << 126
+                    continue
+                assert got == exact, (case, alg, m, n, law)
