@@ -102,3 +102,49 @@ def test_harsh_integer_laws():
                     assert alg == "glynn" and abs(exact) * (1 << (n - 1)) * math.factorial(n - m) >= 1 << 126
                     continue
                 assert got == exact, (case, alg, m, n, law)
+
+
+def test_harsh_batches():
+    """The batch entry points on the same laws: Laplace 8x8, set partitions
+    (m <= 4 < n), thread- and warp-per-matrix Glynn / Ryser, segmented walks."""
+    rng = np.random.default_rng(20261025)
+    shapes = [(8, 8), (4, 10), (3, 7), (2, 12), (5, 5), (6, 9), (12, 12), (7, 14), (1, 6), (16, 16), (5, 8)]
+    for case in range(int(os.environ.get("PERM_FUZZ_HARSH", "120")) // 4):
+        m, n = shapes[case % len(shapes)]
+        B = int(rng.integers(1, 200))
+        cplx = case % 3 == 2
+        A = np.stack([harsh(rng, m, n, (case + i) % 8) + (1j * harsh(rng, m, n, i % 8) if cplx else 0)
+                      for i in range(B)])
+        ref_alg = "combinatoric" if math.perm(n, m) <= 500_000 else ("ryser" if m < n else "glynn")
+        picks = sorted(set(int(i) for i in rng.integers(0, B, 5)) | {0, B - 1})
+        for bfn in (P.opt_batch, P.glynn_batch, P.ryser_batch):
+            out = bfn(A)
+            assert out.shape == (B,)
+            for i in picks:
+                r = O.dd_permanent(ref_alg if ref_alg != "combinatoric" else ("ryser" if m < n else "glynn"),
+                                   A[i], nthreads=1)
+                assert scaled_err(out[i], r, magsum2(A[i])) <= TOL, (case, bfn.__name__, m, n, i, out[i], r)
+
+
+def test_harsh_medium_and_views():
+    """15 <= n <= 22 on the harsh laws, from non-contiguous views, Fortran
+    order, tall inputs (m > n) and strided CUDA tensors."""
+    import torch
+
+    rng = np.random.default_rng(20261026)
+    for case in range(max(6, int(os.environ.get("PERM_FUZZ_HARSH", "120")) // 10)):
+        n = int(rng.integers(15, 23))
+        m = int(rng.integers(n - 5, n + 1))
+        big = harsh(rng, 2 * m, 2 * n, case % 8)
+        if case % 3 == 1:
+            big = big + 1j * harsh(rng, 2 * m, 2 * n, (case + 3) % 8)
+        view = big[::2, 1::2]  # strided, not contiguous
+        a = np.ascontiguousarray(view)
+        ref = O.dd_permanent("ryser" if m < n else "glynn", a, nthreads=16)
+        M = magsum2(a)
+        forms = {"view": view, "fortran": np.asfortranarray(a), "tall": a.T,
+                 "cuda": torch.tensor(big, device="cuda")[::2, 1::2]}
+        for name, x in forms.items():
+            for fn in (P.opt, P.glynn, P.ryser):
+                got = fn(x)
+                assert scaled_err(got, ref, M) <= TOL, (case, name, fn.__name__, m, n, got, ref)
