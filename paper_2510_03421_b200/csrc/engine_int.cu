@@ -458,8 +458,19 @@ static int wrap_range_f32(const IntSetup& s, const F32Quads& g, uint64_t k0, uin
   }
   const uint64_t max_blocks = (uint64_t)nsm * resident;
   const uint64_t lanes = max_blocks * kInt32Threads;
+  // chunk length: the slowest lane walks ceil(chunks / lanes) chunks of L
+  // steps plus a seed worth ~8 steps (B/2 divergent row adds, the chunk's
+  // double-double fold); take the cheapest L
   int log2L = 3;
-  while (log2L < 14 && log2L < amax && (steps >> (log2L + 1)) >= 16 * lanes) ++log2L;
+  double best = 1e300;
+  for (int r = 3; r <= 14 && r <= amax; ++r) {
+    const uint64_t nch = steps >> r;
+    const double cost = (double)((nch + lanes - 1) / lanes) * ((double)(1ull << r) + 8.0);
+    if (cost < best * 0.999) {
+      best = cost;
+      log2L = r;
+    }
+  }
   const uint64_t nchunks = steps >> log2L;
   const uint64_t blocks = std::min<uint64_t>((nchunks + kInt32Threads - 1) / kInt32Threads, max_blocks);
   const int P4 = 4 * g.nq;
