@@ -298,8 +298,14 @@ def exact_int128(alg: str, a, nthreads=None) -> int:
     m, n = a.shape
     s = walk_setup(alg, a)
     total = walk_i128_mt(s, nthreads=nthreads)
+    # The int128 walk wraps silently.  Guard with the double-double value of
+    # the same walk: refuse when the walk sum (the permanent times Glynn's
+    # 2^(n-1) (n-m)!) is not safely inside int128.
+    denom = (1 << (n - 1)) * math.factorial(n - m) if alg == GLYNN else 1
+    est = abs(dd_permanent(alg, np.asarray(a, dtype=np.float64), nthreads=nthreads)) * float(denom)
+    if not est < 2.0 ** 126:
+        raise OverflowError(f"oracle: the {alg} int128 walk sum (~{est:.3e}) does not fit; use the other algorithm")
     if alg == GLYNN:
-        denom = (1 << (n - 1)) * math.factorial(n - m)
         assert total % denom == 0
         return total // denom
     if m == n:
