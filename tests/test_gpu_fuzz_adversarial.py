@@ -148,3 +148,21 @@ def test_harsh_medium_and_views():
             for fn in (P.opt, P.glynn, P.ryser):
                 got = fn(x)
                 assert scaled_err(got, ref, M) <= TOL, (case, name, fn.__name__, m, n, got, ref)
+
+
+def test_full_size_laplace_expansions():
+    """C5 (36x36 f64), C3a (24x24 c128) and C3b (20x28 c128, rectangular) at
+    full size against their own Laplace expansion along a row: n minors, each
+    an independent walk of one size less (for m < n the minor drops the row
+    and one column).  A size-independent check that shares no walk with the
+    value it checks; tolerance 1e-10 relative to sum_j |a_0j per(minor_j)|."""
+    from paper_2510_03421_b200 import workloads as W
+
+    for name, a in (("c5", W.c5(36)), ("c3a", W.c3a()), ("c3b", W.c3b())):
+        m, n = a.shape
+        per = P.glynn(a)
+        rest = a[1:]
+        terms = [a[0, j] * P.glynn(np.ascontiguousarray(np.delete(rest, j, axis=1))) for j in range(n)]
+        lap = sum(terms)
+        scale = sum(abs(t) for t in terms)
+        assert abs(lap - per) <= TOL * scale, (name, per, lap, abs(lap - per) / scale)

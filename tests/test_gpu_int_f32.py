@@ -179,3 +179,32 @@ def test_rectangular_glynn_small_integers_stay_exact():
         if not ovf:
             assert P.glynn(b) == ref, b
         assert P.glynn(b, exact="int128") == O.exact_int128("ryser", b), b
+
+
+def test_c4_full_size_properties():
+    """C4a / C4b at full size through size-independent properties of the
+    permanent, all exact integers: Laplace expansion along a row (n minors of
+    size n - 1, each its own exact walk), invariance under row / column
+    permutations and transposition, multilinearity in a row."""
+    rng = np.random.default_rng(4)
+    for a in (W.c4a(), W.c4b()):
+        n = a.shape[0]
+        per = P.glynn(a, exact="int128")
+        row = int(rng.integers(0, n))
+        rest = np.delete(a, row, axis=0)
+        lap = 0
+        for j in range(n):
+            if a[row, j]:
+                lap += int(a[row, j]) * P.glynn(np.ascontiguousarray(np.delete(rest, j, axis=1)), exact="int128")
+        assert lap == per
+        pr, pc = rng.permutation(n), rng.permutation(n)
+        assert P.glynn(np.ascontiguousarray(a[pr][:, pc]), exact="int128") == per
+        assert P.glynn(np.ascontiguousarray(a.T), exact="int128") == per
+        b = a.copy()
+        b[row] *= 3
+        assert P.glynn(b, exact="int128") == 3 * per
+        c = a.copy()
+        c[row] = rng.integers(0, 2, n)
+        d = a.copy()
+        d[row] = a[row] + c[row]
+        assert P.glynn(d, exact="int128") == per + P.glynn(c, exact="int128")
