@@ -92,7 +92,10 @@ def test_harsh_integer_laws():
                     fn(a)
             else:
                 assert fn(a) == want, (case, alg, m, n, law)
-        exact = O.exact_int128("ryser", a)
+        try:
+            exact = O.exact_int128("ryser", a)
+        except OverflowError:  # the permanent itself leaves int128 (the oracle refuses to wrap)
+            exact = 1 << 127
         if abs(exact) < 1 << 90:
             for alg in algs:
                 try:
