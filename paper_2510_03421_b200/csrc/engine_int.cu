@@ -486,6 +486,8 @@ static int wrap_range_f32(const IntSetup& s, const F32Quads& g, uint64_t k0, uin
   IntWalk32Args a;
   a.v0 = reinterpret_cast<const float*>(base);
   a.U = a.v0 + P4;
+  for (int j = 0; j < 2 * kInt32MaxQuads; ++j)  // row 0 of U as packed pairs (kernel parameter)
+    a.row0[j] = 2 * j + 1 < P4 ? make_float2(buf[(size_t)P4 + 2 * j], buf[(size_t)P4 + 2 * j + 1]) : make_float2(0.f, 0.f);
   a.B = s.B;
   a.log2L = log2L;
   a.escale = std::ldexp(1.0f, -g.scale_log2);

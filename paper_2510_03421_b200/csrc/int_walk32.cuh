@@ -22,44 +22,34 @@
 
 namespace permb200 {
 
+constexpr int kInt32MaxQuads = 10;  // state length <= 40
 struct IntWalk32Args {
   const float* v0;  // [4 NQ] exact integers, pad entries 1
   const float* U;   // [B][4 NQ] exact integers, pad entries 0
+  // row 0 of U (flipped every other step), read as uniform-register operands.  (Rows 1 and 2 as
+  // parameters too: ptxas runs out of uniform registers, hoists them into vector registers, 164 regs.)
+  float2 row0[2 * kInt32MaxQuads];
   int B, log2L;
   float escale;     // 2^-s applied to the estimate product
   uint64_t k_begin, nchunks;
   int64_t* out;     // [blocks][8]: int128 sum, dd estimate (scaled), magnitude (scaled)
 };
 
-using f32x2 = unsigned long long;
+// Packed pairs through the sm_100 float2 intrinsics (FADD2 / FMUL2 / FFMA2):
+// unlike inline PTX they let ptxas take an operand from the uniform
+// registers / the constant bank (row 0 of U arrives as a kernel parameter),
+// which spares the vector register file's read ports -- the quad walk is
+// bound by instruction dispatch, not by a pipe.
+using f32x2 = float2;
 
-__device__ __forceinline__ f32x2 f2_add(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 f2_sub(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 f2_mul(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c) {
-  f32x2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ f32x2 f2_pack(float lo, float hi) {
-  f32x2 d;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
-  return d;
-}
+__device__ __forceinline__ f32x2 f2_add(f32x2 a, f32x2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ f32x2 f2_sub(f32x2 a, f32x2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ f32x2 f2_mul(f32x2 a, f32x2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ f32x2 f2_pack(float lo, float hi) { return make_float2(lo, hi); }
 __device__ __forceinline__ void f2_unpack(f32x2 a, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+  lo = a.x;
+  hi = a.y;
 }
 
 // |x| of an exact FP32 integer below 2^23 as uint32: 2^23 + |x| lies in
@@ -303,25 +293,28 @@ struct Walk32 {
   // Rows are read with volatile shared loads: plain loads of the loop-
   // invariant rows 1 and 2 get hoisted out of the 8-step loop and spill
   // (the same ptxas behaviour as in walk.cuh).  Row 0 lives in registers.
-  static __device__ __forceinline__ ulonglong2 lds2(const f32x2* p) {
-    ulonglong2 u;
-    asm volatile("ld.volatile.shared.v2.b64 {%0, %1}, [%2];"
-                 : "=l"(u.x), "=l"(u.y)
+  struct Pair2 {
+    f32x2 x, y;
+  };
+  static __device__ __forceinline__ Pair2 lds2(const f32x2* p) {
+    Pair2 u;
+    asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(u.x.x), "=f"(u.x.y), "=f"(u.y.x), "=f"(u.y.y)
                  : "r"((unsigned)__cvta_generic_to_shared(p)));
     return u;
   }
-  static __device__ __forceinline__ void reg_add(f32x2 (&v)[NP], const f32x2 (&r)[NP]) {
+  static __device__ __forceinline__ void reg_add(f32x2 (&v)[NP], const f32x2* __restrict__ r) {
 #pragma unroll
     for (int j = 0; j < NP; ++j) v[j] = f2_add(v[j], r[j]);
   }
-  static __device__ __forceinline__ void reg_sub(f32x2 (&v)[NP], const f32x2 (&r)[NP]) {
+  static __device__ __forceinline__ void reg_sub(f32x2 (&v)[NP], const f32x2* __restrict__ r) {
 #pragma unroll
     for (int j = 0; j < NP; ++j) v[j] = f2_sub(v[j], r[j]);
   }
   static __device__ __forceinline__ void row_add(f32x2 (&v)[NP], const f32x2* __restrict__ row) {
 #pragma unroll
     for (int j = 0; j < NP; j += 2) {
-      const ulonglong2 u = lds2(row + j);
+      const Pair2 u = lds2(row + j);
       v[j] = f2_add(v[j], u.x);
       v[j + 1] = f2_add(v[j + 1], u.y);
     }
@@ -329,7 +322,7 @@ struct Walk32 {
   static __device__ __forceinline__ void row_sub(f32x2 (&v)[NP], const f32x2* __restrict__ row) {
 #pragma unroll
     for (int j = 0; j < NP; j += 2) {
-      const ulonglong2 u = lds2(row + j);
+      const Pair2 u = lds2(row + j);
       v[j] = f2_sub(v[j], u.x);
       v[j + 1] = f2_sub(v[j + 1], u.y);
     }
@@ -337,7 +330,7 @@ struct Walk32 {
   static __device__ __forceinline__ void row_fma(f32x2 (&v)[NP], f32x2 s, const f32x2* __restrict__ row) {
 #pragma unroll
     for (int j = 0; j < NP; j += 2) {
-      const ulonglong2 u = lds2(row + j);
+      const Pair2 u = lds2(row + j);
       v[j] = f2_fma(s, u.x, v[j]);
       v[j + 1] = f2_fma(s, u.y, v[j + 1]);
     }
@@ -412,11 +405,11 @@ struct Walk32 {
 
 constexpr int kInt32Threads = 128;
 #ifndef INT32_MINB
-#define INT32_MINB 3
+#define INT32_MINB 4
 #endif
 
 template <int NQ, bool DL4>
-__global__ void __launch_bounds__(kInt32Threads, INT32_MINB) int_walk_wrap_f32_kernel(IntWalk32Args a) {
+__global__ void __launch_bounds__(kInt32Threads, INT32_MINB) int_walk_wrap_f32_kernel(const __grid_constant__ IntWalk32Args a) {
   using W = Walk32<NQ, DL4>;
   constexpr int NP = W::NP;
   extern __shared__ __align__(16) unsigned char smem_raw32[];
@@ -434,9 +427,7 @@ __global__ void __launch_bounds__(kInt32Threads, INT32_MINB) int_walk_wrap_f32_k
   uint32_t acc[4] = {0u, 0u, 0u, 0u};
   double hi = 0.0, lo = 0.0, mag = 0.0;
   const f32x2 one2 = f2_pack(1.0f, 1.0f), mone2 = f2_pack(-1.0f, -1.0f);
-  f32x2 r0[NP];
-#pragma unroll
-  for (int j = 0; j < NP; ++j) r0[j] = sU[j];
+  const f32x2* r0 = a.row0;  // constant-bank operands
   const uint64_t nthr = (uint64_t)gridDim.x * kInt32Threads;
   for (uint64_t c = (uint64_t)blockIdx.x * kInt32Threads + threadIdx.x; c < a.nchunks; c += nthr) {
     const uint64_t k0 = a.k_begin + (c << a.log2L);
@@ -506,7 +497,6 @@ __global__ void __launch_bounds__(kInt32Threads, INT32_MINB) int_walk_wrap_f32_k
 }
 
 using walk_fn_i32 = cudaError_t (*)(const IntWalk32Args&, int blocks, cudaStream_t);
-constexpr int kInt32MaxQuads = 10;  // state length <= 40
 // launcher for NQ quads (nullptr outside 1..kInt32MaxQuads); dl4 = FP64 upper
 // levels; *resident = blocks per SM
 walk_fn_i32 int_wrap_f32_lookup(int NQ, bool dl4, int* resident);

@@ -142,7 +142,10 @@ def test_int128_fuzz():
             a[:, int(rng.integers(0, n))] *= int(rng.integers(1, 2000))  # one heavy column
         # the oracle's int128 walks wrap silently: Ryser's raw sum is the
         # permanent itself, so it is the reference value (|per| < 2^127 here)
-        want = O.exact_int128("ryser", a)
+        try:
+            want = O.exact_int128("ryser", a)
+        except OverflowError:  # the permanent itself is past int128 (the oracle refuses to wrap)
+            continue
         for alg in ("glynn",) + (("ryser",) if m == n else ()):
             try:
                 got = getattr(P, alg)(a, exact="int128")
