@@ -193,6 +193,9 @@ def measure_configs(P, W, torch) -> dict:
     out["C1_glynn_batch_64x12x12"] = {"e2e_ms": 1e3 * wall(lambda: P.glynn_batch(c1), reps=11)}
     for name, A in (("C2a_opt_batch_1e6x8x8", W.c2a()), ("C2b_opt_batch_1e6x4x10", W.c2b())):
         e2e = wall(lambda: P.opt_batch(A), reps=3, warm=1)
+        pA = torch.from_numpy(A).pin_memory()  # page-locked input: the DMA reads it in place
+        e2e_pinned = wall(lambda: P.opt_batch(pA), reps=3, warm=1)
+        del pA
         dA = torch.tensor(A, device="cuda")
         P.opt_batch(dA)
         torch.cuda.synchronize()
@@ -203,7 +206,9 @@ def measure_configs(P, W, torch) -> dict:
         e1.record()
         torch.cuda.synchronize()
         dev_ms = e0.elapsed_time(e1) / 10
-        out[name] = {"e2e_ms": 1e3 * e2e, "device_ms": dev_ms, "hbm_gbs_device": A.nbytes / (dev_ms * 1e-3) / 1e9}
+        out[name] = {"e2e_ms": 1e3 * e2e, "e2e_pinned_ms": 1e3 * e2e_pinned,
+                     "h2d_gbs_pinned": A.nbytes / e2e_pinned / 1e9, "device_ms": dev_ms,
+                     "hbm_gbs_device": A.nbytes / (dev_ms * 1e-3) / 1e9}
         del dA
     c3 = json.loads((ROOT / "tests" / "golden" / "c3.json").read_text())
     for name, a, key in (("C3a_glynn_c128_24x24", W.c3a(), "c3a"), ("C3b_glynn_c128_20x28", W.c3b(), "c3b")):

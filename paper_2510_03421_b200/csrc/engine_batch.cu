@@ -533,6 +533,16 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
   BatchPipe& bp = batch_pipe();
   int st = bp.ensure(in_chunk, out_chunk);
   if (st) return st;
+  // Page-locked input (cudaHostAlloc / cudaHostRegister, e.g. a pinned torch
+  // tensor): the DMA reads the caller's buffer directly, no staging copy.
+  bool pinned_in = false;
+  {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, a) == cudaSuccess)
+      pinned_in = at.type == cudaMemoryTypeHost;
+    else
+      cudaGetLastError();  // an unknown pointer is pageable memory
+  }
   // Results parked in a slot belong to the call that parked them: drop any
   // left behind by an earlier call that returned early, and drop ours on
   // every early return below, so no later call copies stale results into
@@ -558,8 +568,12 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
                   (size_t)bp.pending[slot] * esz);
       bp.pending[slot] = 0;
     }
-    par_memcpy(bp.hin[slot], reinterpret_cast<const char*>(a) + (size_t)c0 * mat_bytes, (size_t)cnt * mat_bytes);
-    PERM_CUDA_TRY(cudaMemcpyAsync(bp.din[slot], bp.hin[slot], (size_t)cnt * mat_bytes, cudaMemcpyHostToDevice,
+    const char* src = reinterpret_cast<const char*>(a) + (size_t)c0 * mat_bytes;
+    if (!pinned_in) {
+      par_memcpy(bp.hin[slot], src, (size_t)cnt * mat_bytes);
+      src = static_cast<const char*>(bp.hin[slot]);
+    }
+    PERM_CUDA_TRY(cudaMemcpyAsync(bp.din[slot], src, (size_t)cnt * mat_bytes, cudaMemcpyHostToDevice,
                                   bp.stream[slot]));
     st = launch_batch(alg, cplx, cnt, m, n, bp.din[slot], bp.dout[slot], bp.stream[slot]);
     if (st) return st;
