@@ -200,6 +200,13 @@ int perm_walk_partial_i64(int alg, int m, int n, const int64_t* a, int64_t lda, 
                           uint64_t k_begin, uint64_t k_end, int64_t* partial, void* stream);
 int perm_walk_finish_i64(int alg, int m, int n, const int64_t* a, int64_t lda, int width, const int64_t* partials,
                          int G, int64_t* out, int* fits_int64);
+/* Host-only planning query (no CUDA call): which exact width-128 walk the
+ * full Gray range of this host matrix takes.  *kind = 4 / 3: quad walk
+ * (FP32 quads under FP64 / integer upper levels), 1: FP64-exact groups,
+ * 0: generic 128-bit state; *groups = quads or FP64 groups per step.  The
+ * walks replace src/_kernels.py:412-523 (glynn_int / ryser_int) and are all
+ * exact; the plan only decides which pipes carry the products. */
+int perm_int_walk_plan(int alg, int m, int n, const int64_t* a, int64_t lda, int* kind, int* groups);
 
 /* ---- single-process multi-device driver (SURVEY 8(b) perm_sharded_*) -----
  * One permanent over `ngpu` devices from one host process: shard i (of

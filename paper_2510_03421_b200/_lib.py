@@ -65,6 +65,7 @@ SIGNATURES = {
                                          C.c_uint64, C.c_int, _vp, C.c_int, _vp]),
     "perm_walk_finish_f64": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, _vp, C.c_int, _dp, _dp]),
     "perm_walk_finish_c128": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, _vp, C.c_int, _dp, _dp]),
+    "perm_int_walk_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "perm_walk_partial_i64": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, C.c_int, C.c_uint64,
                                         C.c_uint64, _ip, _vp]),
     "perm_walk_finish_i64": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int64, C.c_int, _ip, C.c_int, _ip,

@@ -42,6 +42,7 @@ int int_walk_partial(int alg, int m, int n, const int64_t* a, int64_t lda, int d
                      uint64_t k1, int64_t* partial, void* stream);
 int int_walk_finish(int alg, int m, int n, const int64_t* a, int64_t lda, int width, const int64_t* partials, int G,
                     int64_t* out, int* fits_int64);
+int int_walk_plan(int alg, int m, int n, const int64_t* a, int64_t lda, int* kind, int* groups);
 }
 
 namespace {
@@ -804,6 +805,11 @@ int perm_walk_partial_i64(int alg, int m, int n, const int64_t* a, int64_t lda, 
 int perm_walk_finish_i64(int alg, int m, int n, const int64_t* a, int64_t lda, int width, const int64_t* partials,
                          int G, int64_t* out, int* fits_int64) {
   return int_walk_finish(alg, m, n, a, lda, width, partials, G, out, fits_int64);
+}
+
+int perm_int_walk_plan(int alg, int m, int n, const int64_t* a, int64_t lda, int* kind, int* groups) {
+  if (a == nullptr || kind == nullptr || groups == nullptr) return PERM_BAD_ARG;
+  return int_walk_plan(alg, m, n, a, lda, kind, groups);
 }
 
 int perm_sharded_exchange(int ngpu, const int* devices) {

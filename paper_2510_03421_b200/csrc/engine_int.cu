@@ -819,6 +819,34 @@ static int check_int_shardable(int alg, int m, int n, int width) {
   return PERM_OK;
 }
 
+// Host-only: which exact int128 walk the full range of this (host) matrix
+// takes.  kind 4 / 3 = quad walk (FP64 / integer upper levels), 1 =
+// FP64-exact groups, 0 = generic int64 / 128-bit state; groups = quads or
+// FP64 groups.  No CUDA call (CPU tests of the planning logic).
+int int_walk_plan(int alg, int m, int n, const int64_t* a, int64_t lda, int* kind, int* groups) {
+  clear_error();
+  int st = check_int_shardable(alg, m, n, 128);
+  if (st) return st;
+  IntPlan pl;
+  st = load_int_matrix(m, n, a, lda, 0, &pl.A, nullptr);
+  if (st) return st;
+  setup_int(alg, pl.A, &pl.s);
+  const uint64_t k1 = walk_steps(alg, m, n);
+  F32Quads gq;
+  FpGroups g;
+  if (f32_walk_ok(pl.s, 0, k1, &gq)) {
+    *kind = gq.dl4 ? 4 : 3;
+    *groups = gq.nq;
+  } else if (fp_walk_ok(pl.s, 0, k1, &g)) {
+    *kind = 1;
+    *groups = g.ng;
+  } else {
+    *kind = 0;
+    *groups = 0;
+  }
+  return PERM_OK;
+}
+
 int int_walk_partial(int alg, int m, int n, const int64_t* a, int64_t lda, int dev_ptr, int width, uint64_t k0,
                      uint64_t k1, int64_t* partial, void* stream_) {
   clear_error();

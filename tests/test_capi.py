@@ -109,6 +109,57 @@ def test_bad_shapes_rejected_by_the_abi():
     assert lib.perm_walk_shard(2, 3, 3, 2, 2, C.byref(b), C.byref(e)) == _lib.BAD_ARG
 
 
+def _int_plan(alg, a):
+    lib = _lib.load()
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    kind, groups = C.c_int(-1), C.c_int(-1)
+    st = lib.perm_int_walk_plan(alg, a.shape[0], a.shape[1], a.ctypes.data, a.shape[1], C.byref(kind),
+                                C.byref(groups))
+    return st, kind.value, groups.value
+
+
+def test_int_walk_plan_is_host_only_and_follows_the_entry_bounds():
+    """Which exact int128 walk a matrix takes is decided on the host from its
+    column bounds (no CUDA call): C4a / C4b-like matrices take the quad walk,
+    entries past the 23-bit quad / 51-bit group bounds the generic 128-bit
+    state, the weighted (rectangular Ryser) walk always the generic one."""
+    rng = np.random.default_rng(1)
+    c4a = rng.integers(0, 2, (32, 32))
+    c4b = rng.integers(-2, 3, (28, 28))
+    for alg in (1, 2):
+        st, kind, groups = _int_plan(alg, c4a)
+        assert st == _lib.OK and kind in (3, 4) and groups == 8
+    st, kind, groups = _int_plan(2, c4b)
+    assert st == _lib.OK and kind in (3, 4) and groups == 7
+    # the plan depends on the bounds only, not on the values
+    assert _int_plan(2, c4a) == _int_plan(2, np.ones((32, 32)))
+    assert _int_plan(2, rng.integers(-(10**12), 10**12, (24, 24))) == (_lib.OK, 0, 0)
+    assert _int_plan(2, rng.integers(-3, 3, (6, 6))) == (_lib.OK, 0, 0)  # below 8 Gray bits
+    assert _int_plan(1, rng.integers(-3, 3, (10, 20))) == (_lib.OK, 0, 0)  # weighted walk
+    st, kind, groups = _int_plan(2, rng.integers(-3, 3, (10, 20)))  # padded Glynn: 20 state entries
+    assert st == _lib.OK and kind in (3, 4) and groups == 5
+    assert _int_plan(2, np.ones((5, 3)))[0] == _lib.BAD_SHAPE
+    lib = _lib.load()
+    assert lib.perm_int_walk_plan(2, 3, 3, None, 3, None, None) == _lib.BAD_ARG
+
+
+def test_int_walk_plan_quads_can_be_switched_off():
+    code = (
+        "import ctypes as C, numpy as np\n"
+        "from paper_2510_03421_b200 import _lib\n"
+        "lib = _lib.load(); a = np.ones((32, 32), dtype=np.int64)\n"
+        "k, g = C.c_int(), C.c_int()\n"
+        "assert lib.perm_int_walk_plan(2, 32, 32, a.ctypes.data, 32, C.byref(k), C.byref(g)) == 0\n"
+        "print(k.value, g.value)\n"
+    )
+    import os
+    import sys
+
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env={**os.environ, "PERM_INT_F32": "0"},
+                         capture_output=True, text=True, check=True).stdout.split()
+    assert int(out[0]) == 1 and int(out[1]) >= 1  # FP64-exact groups
+
+
 def test_no_cpu_fallback_without_gpu():
     torch = pytest.importorskip("torch")
     if torch.cuda.is_available():
