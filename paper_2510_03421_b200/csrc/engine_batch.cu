@@ -537,11 +537,20 @@ int batch_permanent(int alg, bool cplx, int64_t B, int m, int n, const double* a
   // tensor): the DMA reads the caller's buffer directly, no staging copy.
   bool pinned_in = false;
   {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, a) == cudaSuccess)
-      pinned_in = at.type == cudaMemoryTypeHost;
-    else
-      cudaGetLastError();  // an unknown pointer is pageable memory
+    // both ends of the array must be page-locked (a cudaHostRegister range
+    // may cover only part of it; such input takes the staged route)
+    const char* ends[2] = {reinterpret_cast<const char*>(a),
+                           reinterpret_cast<const char*>(a) + (size_t)B * mat_bytes - 1};
+    pinned_in = true;
+    for (const char* p : ends) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();  // an unknown pointer is pageable memory
+        pinned_in = false;
+      } else if (at.type != cudaMemoryTypeHost) {
+        pinned_in = false;
+      }
+    }
   }
   // Results parked in a slot belong to the call that parked them: drop any
   // left behind by an earlier call that returned early, and drop ours on
