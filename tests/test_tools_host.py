@@ -138,3 +138,32 @@ def test_max_margin_separates():
     assert (y * (X @ w + b)).min() == pytest.approx(1.0)
     w2, b2, cost = svm.min_misclassification_plane(X, y, weights=np.ones(4))
     assert cost == 0 and np.all(y * (X @ w2 + b2) > 0)
+
+
+def test_bench_reference_arm_line_contract():
+    """`bench.py --impl reference` (the CPU arm the driver times beside the
+    engine): one JSON line with the engine arm's metric / unit / config keys,
+    `impl`, a `cpu_baseline` describing the run and an `e2e` repeating the
+    value with zero copy bytes; ranks other than 0 print nothing."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1", "--n", "20"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, check=True).stdout.strip().splitlines()
+    assert len(out) == 1
+    line = json.loads(out[0])
+    assert line["impl"] == "reference" and line["unit"] == "steps/s" and line["higher_is_better"] is True
+    assert line["steps"] == 2 and line["warmup"] == 1 and line["n_gpus"] == 1 and line["dtype"] == "f64"
+    assert line["value"] > 0 and line["ms_per_step"] > 0
+    assert "workload" in line["config"] and "model" not in line["config"]
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
+    assert line["e2e"] == {"value": line["value"], "unit": "steps/s", "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+    env = {**os.environ, "WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"}
+    quiet = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, check=True)
+    assert quiet.stdout.strip() == ""
