@@ -55,3 +55,40 @@ def test_cli_compute(capsys):
     out = capsys.readouterr()
     assert "algorithm:" in out.err and out.out.strip().endswith("i")
     assert cli.main(["compute", "4611686018427387904 3; 5 4611686018427387904"]) == 3
+
+
+def test_bench_engine_line_contract():
+    """`bench.py` on the GPU (a short n = 30 run): one JSON line carrying
+    the driver's keys, the self-check against the committed double-double
+    value, the roofline / cpu_baseline / e2e objects, the launch count and
+    the clock samples."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--n", "30", "--no-configs",
+           "--cpu-seconds", "1"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, check=True).stdout.strip().splitlines()
+    assert len(out) == 1
+    line = json.loads(out[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                "gpu_launches", "clocks"):
+        assert key in line, key
+    assert line["unit"] == "steps/s" and line["n_gpus"] == 1 and line["steps"] == 3 and line["dtype"] == "f64"
+    assert line["vs_baseline"] is None and line["gpu_launches"] >= 3
+    assert line["config"]["value_check"]["checked"] is True and line["config"]["value_check"]["rel_err"] <= 1e-10
+    assert abs(line["value"] - (1 << 29) / (line["ms_per_step"] * 1e-3)) <= 1e-6 * line["value"]
+    rf = line["roofline"]
+    assert 0.5 < rf["frac"] <= 1.02 and abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] == 1 and cb["value"] > 0
+    e2e = line["e2e"]
+    assert e2e["h2d_bytes_per_step"] == 30 * 30 * 8 and e2e["d2h_bytes_per_step"] > 0
+    assert 0 < e2e["value"] <= line["value"] * 1.01
+    clocks = line["clocks"]  # a run this short may end before the first nvidia-smi sample
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(clocks)
+    assert clocks["sm_mhz"] is None or clocks["sm_mhz"] > 0
+    assert not any("slowdown" in r for r in clocks["reasons"])
